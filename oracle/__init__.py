@@ -1,0 +1,277 @@
+"""CPU ORACLE for the SZ-vs-ZFP rate-distortion estimator (arXiv 1806.08901).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  It shares no code with the CUDA path (``paper_1806_08901_b200``);
+neither imports the other.
+
+The arithmetic lives in ``orc.c`` (plain sequential C, fp64 except the fp32
+Lorenzo/quantise decision, R4/R5).  This module only marshals
+arguments through ctypes and compiles ``orc.c`` with gcc on first use.
+
+Parity status: every function is pinned by ``tests/test_oracle_pins.py``
+(closed forms, brute force, invariants, hand examples under ``tests/golden``)
+except the absolute agreement with the real SZ-1.4.11 / ZFP-0.5.0 codecs,
+which is "parity unpinned" (the codecs are not in the container).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "orc.c")
+_HDR = os.path.join(_HERE, "orc.h")
+_LIB = os.path.join(_HERE, "liborc.so")
+_lock = threading.Lock()
+_lib = None
+
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+          "-Wall", "-Wextra"]
+
+NSLOTS = 65536
+OVF_SLOT = 65535
+STATUS = {0: "OK", -1: "EINVAL", -4: "ENONFINITE", -5: "EDEGENERATE"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int):
+        super().__init__(f"oracle status {status} ({STATUS.get(status, '?')})")
+        self.status = status
+
+
+def build(force: bool = False) -> str:
+    """Compile orc.c -> liborc.so (gcc, no fast-math, no FMA contraction)."""
+    stale = (not os.path.exists(_LIB) or
+             os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC), os.path.getmtime(_HDR)))
+    if force or stale:
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class Result(C.Structure):
+    _fields_ = [
+        ("sz_bits_per_value", C.c_double), ("sz_psnr", C.c_double),
+        ("zfp_bits_per_value", C.c_double), ("zfp_psnr", C.c_double),
+        ("choice", C.c_int32), ("matched", C.c_int32),
+        ("value_range", C.c_double), ("eb_abs", C.c_double), ("sz_entropy", C.c_double),
+        ("sz_overflow_frac", C.c_double), ("sz_bits_matched", C.c_double),
+        ("sz_eb_matched", C.c_double), ("zfp_mse", C.c_double),
+        ("n_sz_points", C.c_uint64), ("n_values", C.c_uint64), ("n_blocks", C.c_uint64),
+        ("zfp_total_bits", C.c_uint64), ("zfp_err_sum", C.c_double),
+        ("minexp", C.c_int32), ("r_f", C.c_float),
+    ]
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Debug(C.Structure):
+    _fields_ = [("codes", C.c_void_p), ("hist", C.c_void_p), ("emax", C.c_void_p),
+                ("coef", C.c_void_p), ("uword", C.c_void_p), ("bits", C.c_void_p),
+                ("err", C.c_void_p)]
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_LIB)
+            P = C.c_void_p
+            L.orc_estimate.argtypes = [P, C.c_int, P, C.c_int, C.c_double, P, C.c_double, P, P]
+            L.orc_estimate.restype = C.c_int
+            L.orc_processed_blocks.argtypes = [C.c_int, P, P]
+            L.orc_processed_blocks.restype = C.c_uint64
+            L.orc_lorenzo.argtypes = [P, C.c_int, P, P]
+            L.orc_lorenzo.restype = C.c_float
+            L.orc_quantize.argtypes = [C.c_float, C.c_float]
+            L.orc_quantize.restype = C.c_int32
+            L.orc_entropy_counts.argtypes = [P, C.c_int64]
+            L.orc_entropy_counts.restype = C.c_double
+            for f in ("orc_fwd_lift4", "orc_inv_lift4"):
+                getattr(L, f).argtypes = [P, C.c_int64]
+                getattr(L, f).restype = None
+            for f in ("orc_fwd_xform", "orc_inv_xform"):
+                getattr(L, f).argtypes = [P, C.c_int]
+                getattr(L, f).restype = None
+            L.orc_sequency_perm.argtypes = [C.c_int, P]
+            L.orc_sequency_perm.restype = None
+            L.orc_negabinary.argtypes = [C.c_int32]
+            L.orc_negabinary.restype = C.c_uint32
+            L.orc_negabinary_inv.argtypes = [C.c_uint32]
+            L.orc_negabinary_inv.restype = C.c_int32
+            L.orc_block_emax.argtypes = [P, C.c_int]
+            L.orc_block_emax.restype = C.c_int32
+            L.orc_block_bfp.argtypes = [P, C.c_int, C.c_int32, P]
+            L.orc_block_bfp.restype = None
+            L.orc_precision.argtypes = [C.c_int32, C.c_int32, C.c_int]
+            L.orc_precision.restype = C.c_int32
+            L.orc_gt_count.argtypes = [P, C.c_int, C.c_int]
+            L.orc_gt_count.restype = C.c_uint64
+            L.orc_gt_encode.argtypes = [P, C.c_int, C.c_int, P, C.c_uint64]
+            L.orc_gt_encode.restype = C.c_uint64
+            L.orc_gt_decode.argtypes = [P, C.c_uint64, C.c_int, C.c_int, P]
+            L.orc_gt_decode.restype = C.c_uint64
+            L.orc_block_err.argtypes = [P, P, P, C.c_int, C.c_int, C.c_int32]
+            L.orc_block_err.restype = C.c_double
+            L.orc_gain.argtypes = [C.c_int, C.c_int]
+            L.orc_gain.restype = C.c_double
+            L.orc_select.argtypes = [C.c_double] * 7 + [P, P, P]
+            L.orc_select.restype = C.c_int
+            _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _dims_stride(shape, stride):
+    nd = len(shape)
+    dims = np.ascontiguousarray(shape, dtype=np.int64)
+    st = None if stride is None else np.ascontiguousarray(stride, dtype=np.int32)
+    if st is not None and st.shape != (nd,):
+        raise ValueError("stride must have one entry per dimension")
+    return nd, dims, st
+
+
+def processed_blocks(shape, stride=None) -> int:
+    nd, dims, st = _dims_stride(shape, stride)
+    return int(lib().orc_processed_blocks(nd, _ptr(dims), None if st is None else _ptr(st)))
+
+
+def estimate(x: np.ndarray, eb: float, mode: str = "rel", stride=None, sz_offset: float = 0.5,
+             debug: bool = False) -> dict:
+    """Alg. 1 lines 1-10 on a C-order float32 field."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    nd, dims, st = _dims_stride(x.shape, stride)
+    size = 4 ** nd
+    res = Result()
+    dbgs = None
+    arrays = {}
+    if debug:
+        npb = processed_blocks(x.shape, stride)
+        arrays = {
+            "codes": np.empty(x.shape, np.int32), "hist": np.zeros(NSLOTS, np.uint64),
+            "emax": np.empty(npb, np.int32), "coef": np.empty((npb, size), np.int32),
+            "uword": np.empty((npb, size), np.uint32), "bits": np.empty(npb, np.uint32),
+            "err": np.empty(npb, np.float64),
+        }
+        dbgs = Debug(*[_ptr(arrays[k]) for k, _ in Debug._fields_])
+    st_ = lib().orc_estimate(_ptr(x), nd, _ptr(dims), 1 if mode == "rel" else 0, float(eb),
+                             None if st is None else _ptr(st), float(sz_offset), C.byref(res),
+                             C.byref(dbgs) if dbgs is not None else None)
+    if st_ != 0:
+        raise OracleError(st_)
+    out = res.to_dict()
+    if debug:
+        out["debug"] = arrays
+    return out
+
+
+# ---- single steps (pin tests) ----
+def lorenzo(x: np.ndarray, idx) -> np.float32:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    nd, dims, _ = _dims_stride(x.shape, None)
+    i = np.ascontiguousarray(idx, dtype=np.int64)
+    return np.float32(lib().orc_lorenzo(_ptr(x), nd, _ptr(dims), _ptr(i)))
+
+
+def quantize(d: float, r_f: float) -> int:
+    return int(lib().orc_quantize(float(np.float32(d)), float(np.float32(r_f))))
+
+
+def entropy(counts) -> float:
+    c = np.ascontiguousarray(counts, dtype=np.uint64)
+    return float(lib().orc_entropy_counts(_ptr(c), c.size))
+
+
+def fwd_xform(blk: np.ndarray, nd: int) -> np.ndarray:
+    b = np.ascontiguousarray(blk, dtype=np.int32).copy()
+    assert b.size == 4 ** nd
+    lib().orc_fwd_xform(_ptr(b), nd)
+    return b
+
+
+def inv_xform(blk: np.ndarray, nd: int) -> np.ndarray:
+    b = np.ascontiguousarray(blk, dtype=np.int32).copy()
+    assert b.size == 4 ** nd
+    lib().orc_inv_xform(_ptr(b), nd)
+    return b
+
+
+def sequency_perm(nd: int) -> np.ndarray:
+    p = np.empty(4 ** nd, np.int32)
+    lib().orc_sequency_perm(nd, _ptr(p))
+    return p
+
+
+def negabinary(c: int) -> int:
+    return int(lib().orc_negabinary(int(c)))
+
+
+def negabinary_inv(u: int) -> int:
+    return int(lib().orc_negabinary_inv(int(u) & 0xFFFFFFFF))
+
+
+def block_emax(blk) -> int:
+    b = np.ascontiguousarray(blk, dtype=np.float32)
+    return int(lib().orc_block_emax(_ptr(b), b.size))
+
+
+def block_bfp(blk, emax: int) -> np.ndarray:
+    b = np.ascontiguousarray(blk, dtype=np.float32)
+    o = np.empty(b.size, np.int32)
+    lib().orc_block_bfp(_ptr(b), b.size, int(emax), _ptr(o))
+    return o
+
+
+def precision(emax: int, minexp: int, nd: int) -> int:
+    return int(lib().orc_precision(int(emax), int(minexp), nd))
+
+
+def gt_count(u, kmin: int) -> int:
+    a = np.ascontiguousarray(u, dtype=np.uint32)
+    return int(lib().orc_gt_count(_ptr(a), a.size, int(kmin)))
+
+
+def gt_encode(u, kmin: int) -> tuple[bytes, int]:
+    a = np.ascontiguousarray(u, dtype=np.uint32)
+    cap = 64 * 33 + 64
+    buf = np.zeros((cap + 7) // 8, np.uint8)
+    n = int(lib().orc_gt_encode(_ptr(a), a.size, int(kmin), _ptr(buf), cap))
+    return buf.tobytes(), n
+
+
+def gt_decode(buf: bytes, nbits: int, size: int, kmin: int) -> tuple[np.ndarray, int]:
+    b = np.frombuffer(buf, np.uint8).copy()
+    u = np.zeros(size, np.uint32)
+    n = int(lib().orc_gt_decode(_ptr(b), int(nbits), size, int(kmin), _ptr(u)))
+    return u, n
+
+
+def block_err(coef_nat, u_seq, nd: int, kmin: int, emax: int) -> float:
+    c = np.ascontiguousarray(coef_nat, dtype=np.int32)
+    u = np.ascontiguousarray(u_seq, dtype=np.uint32)
+    p = sequency_perm(nd)
+    return float(lib().orc_block_err(_ptr(c), _ptr(u), _ptr(p), nd, int(kmin), int(emax)))
+
+
+def gain(nd: int, n: int) -> float:
+    return float(lib().orc_gain(nd, n))
+
+
+def select(br_sz, psnr_sz, br_zfp, psnr_zfp, vr, eb_abs, zfp_mse):
+    bm = C.c_double()
+    ebm = C.c_double()
+    m = C.c_int32()
+    ch = lib().orc_select(br_sz, psnr_sz, br_zfp, psnr_zfp, vr, eb_abs, zfp_mse,
+                          C.byref(bm), C.byref(ebm), C.byref(m))
+    return int(ch), bm.value, ebm.value, int(m.value)

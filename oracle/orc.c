@@ -1,0 +1,508 @@
+/*
+ * orc.c -- plain sequential CPU ORACLE (test infrastructure only; see orc.h).
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared
+ *        (x86-64 SSE: float arithmetic is evaluated in float, FLT_EVAL_METHOD 0).
+ * No blocking, fusion or reordering beyond what each cited definition states.
+ * Readings R1..R17 are listed in DESIGN.md section 3.
+ */
+#include "orc.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ */
+/* small helpers                                                        */
+/* ------------------------------------------------------------------ */
+static int64_t ipow4(int d) { int64_t r = 1; while (d-- > 0) r *= 4; return r; }
+
+/* floor(v / 2) for a signed integer, written out (the lifting network's ">>1"). */
+static int64_t floor_half(int64_t v) { return (v >= 0) ? v / 2 : -((1 - v) / 2); }
+
+/* value of x at multi-index idx; 0 outside the field (R4: zero boundary). */
+static float at_or_zero(const float *x, int nd, const int64_t *dims, const int64_t *idx) {
+  int64_t lin = 0;
+  for (int a = 0; a < nd; ++a) {
+    if (idx[a] < 0 || idx[a] >= dims[a]) return 0.0f;
+    lin = lin * dims[a] + idx[a];
+  }
+  return x[lin];
+}
+
+/* ------------------------------------------------------------------ */
+/* A4  Lorenzo residual on ORIGINAL values (P:151 footnote)     */
+/*     nested first differences in fp32 (reading R4)                   */
+/* ------------------------------------------------------------------ */
+float orc_lorenzo(const float *x, int nd, const int64_t *dims, const int64_t *idx) {
+  int64_t t[3];
+  if (nd == 1) {
+    t[0] = idx[0];     float x0 = at_or_zero(x, nd, dims, t);
+    t[0] = idx[0] - 1; float x1 = at_or_zero(x, nd, dims, t);
+    return x0 - x1;
+  }
+  if (nd == 2) {
+    float v[2][2]; /* v[di][dj] = x[i-di][j-dj] */
+    for (int di = 0; di < 2; ++di)
+      for (int dj = 0; dj < 2; ++dj) {
+        t[0] = idx[0] - di; t[1] = idx[1] - dj;
+        v[di][dj] = at_or_zero(x, nd, dims, t);
+      }
+    float r0 = v[0][0] - v[0][1];
+    float r1 = v[1][0] - v[1][1];
+    return r0 - r1;
+  }
+  float v[2][2][2];
+  for (int di = 0; di < 2; ++di)
+    for (int dj = 0; dj < 2; ++dj)
+      for (int dk = 0; dk < 2; ++dk) {
+        t[0] = idx[0] - di; t[1] = idx[1] - dj; t[2] = idx[2] - dk;
+        v[di][dj][dk] = at_or_zero(x, nd, dims, t);
+      }
+  float a = v[0][0][0] - v[0][0][1];
+  float b = v[0][1][0] - v[0][1][1];
+  float c = v[1][0][0] - v[1][0][1];
+  float e = v[1][1][0] - v[1][1][1];
+  return (a - b) - (c - e);
+}
+
+/* ------------------------------------------------------------------ */
+/* A5  linear quantisation, bin width 2*eb, 65,535 bins     */
+/*     (P:637); overflow -> slot 65535 (reading R5)                     */
+/* ------------------------------------------------------------------ */
+int32_t orc_quantize(float d, float r_f) {
+  float q = fabsf(d) * r_f;
+  if (!(q < 32767.5f)) return ORC_OVF_SLOT;
+  int32_t m = (int32_t)lrintf(q); /* round half to even (default FE_TONEAREST) */
+  int32_t code = (d < 0.0f) ? -m : m;
+  return code + 32767;
+}
+
+/* ------------------------------------------------------------------ */
+/* A6  Shannon entropy of bin probabilities, Eq. (entropy)   */
+/*     BR = - sum_i P_i log2 P_i,  P_i = c_i / N                        */
+/* ------------------------------------------------------------------ */
+double orc_entropy_counts(const uint64_t *c, int64_t n) {
+  uint64_t tot = 0;
+  for (int64_t i = 0; i < n; ++i) tot += c[i];
+  if (tot == 0) return 0.0;
+  double H = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (c[i] == 0) continue;
+    double p = (double)c[i] / (double)tot;
+    H -= p * log2(p);
+  }
+  return H;
+}
+
+/* ------------------------------------------------------------------ */
+/* A8  ZFP forward decorrelating lift on one 4-vector (reading R8).    */
+/*     Exact-arithmetic map = A = (1/16)[[4,4,4,4],[5,1,-1,-5],         */
+/*     [-4,4,4,-4],[-2,6,-6,2]]; ">>1" is floor(v/2).                   */
+/* ------------------------------------------------------------------ */
+void orc_fwd_lift4(int32_t *p, int64_t s) {
+  int64_t x = p[0], y = p[s], z = p[2 * s], w = p[3 * s];
+  /* stage 1: x <- (x+w)/2, w <- w - x */
+  x = floor_half(x + w); w = w - x;
+  /* stage 2: z <- (z+y)/2, y <- y - z */
+  z = floor_half(z + y); y = y - z;
+  /* stage 3: x <- (x+z)/2, z <- z - x */
+  x = floor_half(x + z); z = z - x;
+  /* stage 4: w <- (w+y)/2, y <- y - w */
+  w = floor_half(w + y); y = y - w;
+  /* stage 5: w <- w + y/2, y <- y - w/2 */
+  w = w + floor_half(y); y = y - floor_half(w);
+  p[0] = (int32_t)x; p[s] = (int32_t)y; p[2 * s] = (int32_t)z; p[3 * s] = (int32_t)w;
+}
+
+/* inverse network: the five stages undone in reverse order (linear part A^-1) */
+void orc_inv_lift4(int32_t *p, int64_t s) {
+  int64_t x = p[0], y = p[s], z = p[2 * s], w = p[3 * s];
+  y = y + floor_half(w); w = w - floor_half(y);   /* undo stage 5 */
+  y = y + w; w = 2 * w; w = w - y;                /* undo stage 4 */
+  z = z + x; x = 2 * x; x = x - z;                /* undo stage 3 */
+  y = y + z; z = 2 * z; z = z - y;                /* undo stage 2 */
+  w = w + x; x = 2 * x; x = x - w;                /* undo stage 1 */
+  p[0] = (int32_t)x; p[s] = (int32_t)y; p[2 * s] = (int32_t)z; p[3 * s] = (int32_t)w;
+}
+
+/* separable application, fastest axis first (P:218-233 unfold/fold along each
+ * axis; ZFP order x -> y -> z, reading R8).  blk is 4^d int32 row-major. */
+void orc_fwd_xform(int32_t *blk, int nd) {
+  int64_t size = ipow4(nd);
+  for (int a = nd - 1; a >= 0; --a) {
+    int64_t s = ipow4(nd - 1 - a); /* stride of axis a */
+    for (int64_t n = 0; n < size; ++n) {
+      if ((n / s) % 4 != 0) continue; /* line start: coordinate along a == 0 */
+      orc_fwd_lift4(blk + n, s);
+    }
+  }
+}
+
+void orc_inv_xform(int32_t *blk, int nd) {
+  int64_t size = ipow4(nd);
+  for (int a = 0; a < nd; ++a) {
+    int64_t s = ipow4(nd - 1 - a);
+    for (int64_t n = 0; n < size; ++n) {
+      if ((n / s) % 4 != 0) continue;
+      orc_inv_lift4(blk + n, s);
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* A10 total-sequency order: sort multi-indices by (sum i, sum i^2, n)  */
+/*     (reading R10; low frequencies first, the "staircase" P:436)      */
+/* ------------------------------------------------------------------ */
+void orc_sequency_perm(int nd, int32_t *perm) {
+  int size = (int)ipow4(nd);
+  int key1[64], key2[64];
+  for (int n = 0; n < size; ++n) {
+    int s1 = 0, s2 = 0, r = n;
+    for (int a = 0; a < nd; ++a) { int i = r % 4; r /= 4; s1 += i; s2 += i * i; }
+    key1[n] = s1; key2[n] = s2; perm[n] = n;
+  }
+  for (int i = 1; i < size; ++i) { /* insertion sort, stable on n */
+    int32_t v = perm[i]; int j = i - 1;
+    while (j >= 0) {
+      int32_t u = perm[j];
+      int gt = key1[u] > key1[v] || (key1[u] == key1[v] && (key2[u] > key2[v] ||
+               (key2[u] == key2[v] && u > v)));
+      if (!gt) break;
+      perm[j + 1] = u; --j;
+    }
+    perm[j + 1] = v;
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* A11 negabinary (reading R11):  u = (c + 0xAAAAAAAA) xor 0xAAAAAAAA   */
+/* ------------------------------------------------------------------ */
+uint32_t orc_negabinary(int32_t c) {
+  return ((uint32_t)c + 0xAAAAAAAAu) ^ 0xAAAAAAAAu;
+}
+int32_t orc_negabinary_inv(uint32_t u) {
+  return (int32_t)((u ^ 0xAAAAAAAAu) - 0xAAAAAAAAu);
+}
+
+/* ------------------------------------------------------------------ */
+/* A9  block exponent ("alignment of exponent"): max frexp        */
+/*     exponent over nonzero values, clamped >= -126; -127 if empty     */
+/* ------------------------------------------------------------------ */
+int32_t orc_block_emax(const float *blk, int n) {
+  int any = 0, emax = -1000;
+  for (int i = 0; i < n; ++i) {
+    if (blk[i] == 0.0f) continue;
+    int e; frexpf(blk[i], &e);
+    if (!any || e > emax) emax = e;
+    any = 1;
+  }
+  if (!any) return -127;
+  return emax < -126 ? -126 : emax;
+}
+
+/* "fixed-point integer conversion": i = trunc(x * 2^(30-emax)), exact */
+void orc_block_bfp(const float *blk, int n, int32_t emax, int32_t *out) {
+  for (int i = 0; i < n; ++i)
+    out[i] = (int32_t)trunc(ldexp((double)blk[i], 30 - emax));
+}
+
+/* A12 fixed-accuracy precision (reading R12; ZFP-0.5 fixed accuracy P:507) */
+int32_t orc_precision(int32_t emax, int32_t minexp, int nd) {
+  int64_t p = (int64_t)emax - minexp + 2 * (nd + 1);
+  if (p < 0) p = 0;
+  if (p > 32) p = 32;
+  return (int32_t)p;
+}
+
+/* ------------------------------------------------------------------ */
+/* A13 group-testing embedded coder (EC; reading R13),    */
+/*     simulated literally: planes 31..kmin, n carried across planes.   */
+/* ------------------------------------------------------------------ */
+static int plane_bit(const uint32_t *u, int j, int k) { return (int)((u[j] >> k) & 1u); }
+
+uint64_t orc_gt_count(const uint32_t *u, int size, int kmin) {
+  uint64_t bits = 0;
+  int n = 0;
+  for (int k = 31; k >= kmin; --k) {
+    bits += (uint64_t)n;                       /* (i) verbatim bits of 0..n-1 */
+    while (n < size) {                         /* (ii) group tests            */
+      int any = 0;
+      for (int j = n; j < size; ++j) any |= plane_bit(u, j, k);
+      bits += 1;
+      if (!any) break;
+      for (;;) {
+        if (n == size - 1) { n = size; break; }  /* last 1 implied */
+        bits += 1;
+        int b = plane_bit(u, n, k);
+        ++n;
+        if (b) break;
+      }
+    }
+  }
+  return bits;
+}
+
+static void put_bit(uint8_t *buf, uint64_t pos, int b) {
+  if (b) buf[pos >> 3] |= (uint8_t)(1u << (pos & 7));
+  else buf[pos >> 3] &= (uint8_t)~(1u << (pos & 7));
+}
+static int get_bit(const uint8_t *buf, uint64_t pos) { return (buf[pos >> 3] >> (pos & 7)) & 1; }
+
+/* actually write the EC bitstream; returns its length in bits (0 on overflow) */
+uint64_t orc_gt_encode(const uint32_t *u, int size, int kmin, uint8_t *buf, uint64_t cap) {
+  uint64_t pos = 0;
+  int n = 0;
+#define PUT(b) do { if (pos >= cap) return 0; put_bit(buf, pos++, (b)); } while (0)
+  for (int k = 31; k >= kmin; --k) {
+    for (int j = 0; j < n; ++j) PUT(plane_bit(u, j, k));
+    while (n < size) {
+      int any = 0;
+      for (int j = n; j < size; ++j) any |= plane_bit(u, j, k);
+      PUT(any);
+      if (!any) break;
+      for (;;) {
+        if (n == size - 1) { n = size; break; }
+        int b = plane_bit(u, n, k);
+        PUT(b);
+        ++n;
+        if (b) break;
+      }
+    }
+  }
+#undef PUT
+  return pos;
+}
+
+/* decode the stream back into words (bits below kmin are zero); returns bits read */
+uint64_t orc_gt_decode(const uint8_t *buf, uint64_t nbits, int size, int kmin, uint32_t *u) {
+  uint64_t pos = 0;
+  int n = 0;
+  for (int j = 0; j < size; ++j) u[j] = 0;
+#define GET() ((pos < nbits) ? get_bit(buf, pos++) : (pos++, 0))
+  for (int k = 31; k >= kmin; --k) {
+    for (int j = 0; j < n; ++j) if (GET()) u[j] |= 1u << k;
+    while (n < size) {
+      if (!GET()) break;
+      for (;;) {
+        if (n == size - 1) { u[n] |= 1u << k; n = size; break; }
+        int b = GET();
+        if (b) u[n] |= 1u << k;
+        ++n;
+        if (b) break;
+      }
+    }
+  }
+#undef GET
+  return pos;
+}
+
+/* ------------------------------------------------------------------ */
+/* A14 truncation error weighted by the squared column norms of the     */
+/*     inverse transform (reading R14, Theorem thm:1 P:275)  */
+/* ------------------------------------------------------------------ */
+double orc_gain(int nd, int n) {
+  static const double g[4] = {4.0, 5.0, 4.0, 3.25};
+  double w = 1.0;
+  for (int a = 0; a < nd; ++a) { w *= g[n % 4]; n /= 4; }
+  return w;
+}
+
+double orc_block_err(const int32_t *coef_nat, const uint32_t *u_seq, const int32_t *perm,
+                     int nd, int kmin, int32_t emax) {
+  int size = (int)ipow4(nd);
+  double E = 0.0;
+  for (int j = 0; j < size; ++j) {
+    uint32_t ut = (kmin >= 32) ? 0u : (u_seq[j] & ~((1u << kmin) - 1u));
+    int32_t ct = orc_negabinary_inv(ut);
+    int64_t e = (int64_t)coef_nat[perm[j]] - (int64_t)ct;
+    double ed = (double)e;
+    E += orc_gain(nd, perm[j]) * (ed * ed);
+  }
+  return E * ldexp(1.0, 2 * (emax - 30));
+}
+
+/* ------------------------------------------------------------------ */
+/* A16 selection, Alg. 1 lines 7-10, ties -> ZFP            */
+/* ------------------------------------------------------------------ */
+int orc_select(double br_sz, double psnr_sz, double br_zfp, double psnr_zfp,
+               double vr, double eb_abs, double zfp_mse, double *bm, double *ebm,
+               int32_t *matched) {
+  (void)psnr_sz;
+  if (!(zfp_mse > 0.0) || !(vr > 0.0) || !isfinite(psnr_zfp)) {
+    /* reading R16(ii): matching impossible -> compare at the user's eb */
+    *matched = 0; *bm = br_sz; *ebm = eb_abs;
+    return (br_sz < br_zfp) ? 0 : 1;
+  }
+  /* line 7: delta from PSNR_sz = PSNR_zfp with Eq. (psnr-pdf-linear) */
+  double delta = vr * sqrt(12.0) * pow(10.0, -psnr_zfp / 20.0);
+  /* lines 8-9: Eq. (bitrate-sz) evaluated with the 2eb-histogram density
+   * (reading R16(i)):  BR(delta) = BR(2eb) + log2(2eb / delta) */
+  double b = br_sz + log2(2.0 * eb_abs / delta);
+  if (b < 0.0) b = 0.0;
+  *matched = 1; *bm = b; *ebm = delta / 2.0;
+  return (b < br_zfp) ? 0 : 1;   /* line 10: IF BR_sz < BR_zfp -> SZ */
+}
+
+/* ------------------------------------------------------------------ */
+/* A3 block sampling: block b processed iff b_a % s_a == 0  */
+/* ------------------------------------------------------------------ */
+uint64_t orc_processed_blocks(int nd, const int64_t *dims, const int32_t *stride) {
+  uint64_t r = 1;
+  for (int a = 0; a < nd; ++a) {
+    int64_t nb = (dims[a] + 3) / 4;
+    int64_t s = stride ? stride[a] : 1;
+    r *= (uint64_t)((nb + s - 1) / s);
+  }
+  return r;
+}
+
+/* ------------------------------------------------------------------ */
+/* whole field: Alg. 1 lines 1-10                                       */
+/* ------------------------------------------------------------------ */
+int orc_estimate(const float *x, int nd, const int64_t *dims, int eb_mode, double eb,
+                 const int32_t *stride, double sz_offset, orc_result *out, orc_debug *dbg) {
+  if (nd < 1 || nd > 3 || !x || !dims || !out) return ORC_EINVAL;
+  int64_t N = 1;
+  for (int a = 0; a < nd; ++a) { if (dims[a] < 1) return ORC_EINVAL; N *= dims[a]; }
+  int32_t s[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) { s[a] = stride ? stride[a] : 1; if (s[a] < 1) return ORC_EINVAL; }
+  if (!isfinite(eb) || !(eb > 0.0)) return ORC_EINVAL;
+  if (eb_mode != 0 && eb_mode != 1) return ORC_EINVAL;
+
+  /* A1: value range over the whole field */
+  float vmin = x[0], vmax = x[0];
+  for (int64_t i = 0; i < N; ++i) {
+    if (!isfinite(x[i])) return ORC_ENONFINITE;
+    if (x[i] < vmin) vmin = x[i];
+    if (x[i] > vmax) vmax = x[i];
+  }
+  double VR = (double)vmax - (double)vmin;
+
+  /* A2: error bound (Alg. 1 line 2) and derived scalars */
+  double eb_abs = (eb_mode == 1) ? eb * VR : eb;
+  if (eb_mode == 1 && VR == 0.0) return ORC_EDEGENERATE;
+  float r_f = (float)(1.0 / (2.0 * eb_abs));
+  if (!isfinite(r_f) || !(eb_abs > 0.0)) return ORC_EINVAL;
+  int fe; frexp(eb_abs, &fe);
+  int32_t minexp = fe - 1; /* floor(log2 eb_abs) */
+
+  int64_t nb[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) nb[a] = (dims[a] + 3) / 4;
+  int size = (int)ipow4(nd);
+  int32_t perm[64];
+  orc_sequency_perm(nd, perm);
+
+  uint64_t *hist = (uint64_t *)calloc(ORC_NSLOTS, sizeof(uint64_t));
+  if (!hist) return ORC_EINVAL;
+  if (dbg && dbg->codes) for (int64_t i = 0; i < N; ++i) dbg->codes[i] = -1;
+
+  uint64_t n_sz = 0, n_values = 0, n_blocks = 0, total_bits = 0;
+  double err_sum = 0.0;
+  int64_t pb = 0; /* processed-block ordinal */
+
+  int64_t b[3];
+  int64_t nblk_total = nb[0] * nb[1] * nb[2];
+  for (int64_t lb = 0; lb < nblk_total; ++lb) {
+    /* block coordinates, row-major (axis 0 slowest) */
+    int64_t r = lb;
+    for (int a = nd - 1; a >= 0; --a) { b[a] = r % nb[a]; r /= nb[a]; }
+    int processed = 1;
+    for (int a = 0; a < nd; ++a) if (b[a] % s[a] != 0) processed = 0;
+    if (!processed) continue;
+
+    /* ---- SZ part: A4-A5 for every real point of the block ---- */
+    float blk[64];
+    int nreal = 0;
+    for (int n = 0; n < size; ++n) {
+      int64_t idx[3], cl[3];
+      int inside = 1, rr = n;
+      for (int a = nd - 1; a >= 0; --a) {
+        int o = rr % 4; rr /= 4;
+        idx[a] = 4 * b[a] + o;
+        if (idx[a] >= dims[a]) inside = 0;
+        cl[a] = idx[a] < dims[a] ? idx[a] : dims[a] - 1; /* edge replication (R17) */
+      }
+      int64_t lin = 0;
+      for (int a = 0; a < nd; ++a) lin = lin * dims[a] + cl[a];
+      blk[n] = x[lin];
+      if (!inside) continue;
+      ++nreal;
+      int origin = 1;
+      for (int a = 0; a < nd; ++a) if (idx[a] != 0) origin = 0;
+      if (origin) continue; /* R4: the first value is stored verbatim */
+      float d = orc_lorenzo(x, nd, dims, idx);
+      int32_t slot = orc_quantize(d, r_f);
+      hist[slot] += 1;
+      ++n_sz;
+      if (dbg && dbg->codes) dbg->codes[lin] = slot;
+    }
+    n_values += (uint64_t)nreal;
+    ++n_blocks;
+
+    /* ---- ZFP part: A9-A14 on the (padded) block ---- */
+    int32_t emax = orc_block_emax(blk, size);
+    int32_t coef[64];
+    uint32_t u[64];
+    uint64_t bits;
+    double E;
+    if (emax == -127) { /* empty block: 1 header bit, no error */
+      for (int n = 0; n < size; ++n) { coef[n] = 0; u[n] = 0; }
+      bits = 1; E = 0.0;
+    } else {
+      orc_block_bfp(blk, size, emax, coef);
+      orc_fwd_xform(coef, nd);
+      for (int j = 0; j < size; ++j) u[j] = orc_negabinary(coef[perm[j]]);
+      int32_t p = orc_precision(emax, minexp, nd);
+      int kmin = 32 - p;
+      bits = (p == 0) ? 1 : 9 + orc_gt_count(u, size, kmin);
+      E = orc_block_err(coef, u, perm, nd, kmin, emax);
+    }
+    total_bits += bits;
+    err_sum += E;
+    if (dbg) {
+      if (dbg->emax) dbg->emax[pb] = emax;
+      if (dbg->coef) memcpy(dbg->coef + pb * size, coef, sizeof(int32_t) * size);
+      if (dbg->uword) memcpy(dbg->uword + pb * size, u, sizeof(uint32_t) * size);
+      if (dbg->bits) dbg->bits[pb] = (uint32_t)bits;
+      if (dbg->err) dbg->err[pb] = E;
+    }
+    ++pb;
+  }
+
+  if (n_sz == 0) { free(hist); return ORC_EDEGENERATE; }
+
+  /* A6: entropy bit-rate (Eq. entropy, bitrate-sz P:402), +0.5 offset */
+  double H = orc_entropy_counts(hist, ORC_NSLOTS);
+  double p_ovf = (double)hist[ORC_OVF_SLOT] / (double)n_sz;
+  double br_sz = H + sz_offset + 32.0 * p_ovf;
+  /* A7: Eq. (psnr-sz) */
+  double psnr_sz = 20.0 * log10(VR / eb_abs) + 10.0 * log10(3.0);
+  /* A13/A15: EC bit-rate; A14 PSNR_sp */
+  double br_zfp = (double)total_bits / (double)n_values;
+  double mse = err_sum / (double)n_values;
+  double psnr_zfp = (mse > 0.0) ? 20.0 * log10(VR) - 10.0 * log10(mse) : INFINITY;
+
+  memset(out, 0, sizeof(*out));
+  out->sz_bits_per_value = br_sz;
+  out->sz_psnr = psnr_sz;
+  out->zfp_bits_per_value = br_zfp;
+  out->zfp_psnr = psnr_zfp;
+  out->value_range = VR;
+  out->eb_abs = eb_abs;
+  out->sz_entropy = H;
+  out->sz_overflow_frac = p_ovf;
+  out->zfp_mse = mse;
+  out->n_sz_points = n_sz;
+  out->n_values = n_values;
+  out->n_blocks = n_blocks;
+  out->zfp_total_bits = total_bits;
+  out->zfp_err_sum = err_sum;
+  out->minexp = minexp;
+  out->r_f = r_f;
+  out->choice = orc_select(br_sz, psnr_sz, br_zfp, psnr_zfp, VR, eb_abs, mse,
+                           &out->sz_bits_matched, &out->sz_eb_matched, &out->matched);
+  if (dbg && dbg->hist) memcpy(dbg->hist, hist, sizeof(uint64_t) * ORC_NSLOTS);
+  free(hist);
+  return ORC_OK;
+}

@@ -1,0 +1,88 @@
+/*
+ * orc.h -- CPU ORACLE for the SZ-vs-ZFP rate-distortion estimator of
+ * Tao, Di, Liang, Chen, Cappello, "Optimizing Lossy Compression
+ * Rate-Distortion from Automatic Online Selection between SZ and ZFP"
+ * (arXiv 1806.08901, IEEE TPDS 2018), PAPER.md.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1806_08901_b200/, include/sel.h) never links,
+ * includes or calls anything here, and this file includes nothing from it.
+ *
+ * Every routine is a plain, sequential restatement of one step of the paper
+ * (or of a DESIGN.md "reading" where the paper is silent); citations are
+ * "P:<line>" into PAPER.md.  Floating point: fp64 except where the decision
+ * that yields an integer is taken in fp32 on both sides (Lorenzo residual and
+ * quantisation, R4/R5).
+ */
+#ifndef ORC_H
+#define ORC_H
+#include <stdint.h>
+
+#define ORC_OK 0
+#define ORC_EINVAL -1
+#define ORC_ENONFINITE -4
+#define ORC_EDEGENERATE -5
+
+#define ORC_NSLOTS 65536       /* 65,535 code bins + 1 overflow slot */
+#define ORC_OVF_SLOT 65535
+
+typedef struct {
+  double sz_bits_per_value, sz_psnr, zfp_bits_per_value, zfp_psnr;
+  int32_t choice, matched;
+  double value_range, eb_abs, sz_entropy, sz_overflow_frac;
+  double sz_bits_matched, sz_eb_matched, zfp_mse;
+  uint64_t n_sz_points, n_values, n_blocks, zfp_total_bits;
+  double zfp_err_sum;   /* sum_b E_b (value units squared) */
+  int32_t minexp;
+  float r_f;
+} orc_result;
+
+/* Optional per-element dumps (any pointer may be NULL).
+ * codes      : int32[N]   slot of every SZ point, -1 where no code was formed
+ * hist       : uint64[65536]
+ * emax       : int32[NP]  per processed block (row-major over processed blocks); -127 = empty
+ * coef       : int32[NP*4^d] lifted coefficients, natural (row-major) order
+ * uword      : uint32[NP*4^d] negabinary words in sequency order
+ * bits       : uint32[NP]
+ * err        : double[NP] E_b in value units squared                      */
+typedef struct {
+  int32_t *codes;
+  uint64_t *hist;
+  int32_t *emax;
+  int32_t *coef;
+  uint32_t *uword;
+  uint32_t *bits;
+  double *err;
+} orc_debug;
+
+/* ---- whole-field estimate (Alg. 1 lines 1-10) ---- */
+int orc_estimate(const float *x, int ndims, const int64_t *dims, int eb_mode,
+                 double eb, const int32_t *stride, double sz_offset,
+                 orc_result *out, orc_debug *dbg);
+uint64_t orc_processed_blocks(int ndims, const int64_t *dims, const int32_t *stride);
+
+/* ---- single steps, exported for the pin tests ---- */
+float orc_lorenzo(const float *x, int ndims, const int64_t *dims, const int64_t *idx);
+int32_t orc_quantize(float d, float r_f);
+double orc_entropy_counts(const uint64_t *c, int64_t n);
+void orc_fwd_lift4(int32_t *v, int64_t stride);
+void orc_inv_lift4(int32_t *v, int64_t stride);
+void orc_fwd_xform(int32_t *blk, int ndims);
+void orc_inv_xform(int32_t *blk, int ndims);
+void orc_sequency_perm(int ndims, int32_t *perm);
+uint32_t orc_negabinary(int32_t c);
+int32_t orc_negabinary_inv(uint32_t u);
+int32_t orc_block_emax(const float *blk, int n);
+void orc_block_bfp(const float *blk, int n, int32_t emax, int32_t *out);
+int32_t orc_precision(int32_t emax, int32_t minexp, int ndims);
+uint64_t orc_gt_count(const uint32_t *u, int n, int kmin);
+uint64_t orc_gt_encode(const uint32_t *u, int n, int kmin, uint8_t *buf, uint64_t cap_bits);
+uint64_t orc_gt_decode(const uint8_t *buf, uint64_t nbits, int n, int kmin, uint32_t *u);
+double orc_block_err(const int32_t *coef_nat, const uint32_t *u_seq, const int32_t *perm,
+                     int ndims, int kmin, int32_t emax);
+double orc_gain(int ndims, int nat_index);
+int orc_select(double br_sz, double psnr_sz, double br_zfp, double psnr_zfp,
+               double vr, double eb_abs, double zfp_mse, double *br_sz_matched,
+               double *eb_sz_matched, int32_t *matched);
+#endif
