@@ -1,0 +1,158 @@
+/*
+ * sel.h -- C ABI of the B200-native SZ-vs-ZFP rate-distortion estimator.
+ *
+ * Implements the hot path of Tao et al., "Optimizing Lossy Compression
+ * Rate-Distortion from Automatic Online Selection between SZ and ZFP"
+ * (arXiv 1806.08901): Algorithm 1 lines 1-10 for one
+ * float32 field resident in GPU memory:
+ *   - value range VR and eb = eb_abs or eb_rel*VR            (Alg.1 line 2)
+ *   - block sampling with per-axis stride                      (Alg.1 line 3)
+ *   - SZ: Lorenzo residual on original values, linear
+ *     quantisation with bin width 2*eb, histogram of codes with
+ *     65,535 bins, Shannon-entropy bit-rate (Eq. entropy P:326,
+ *     Eq. bitrate-sz) + 0.5 bit offset, PSNR Eq. psnr-sz
+ *   - ZFP: per 4^d block exponent, block floating point, decorrelating lift,
+ *     sequency reorder, negabinary, exact group-testing EC bit count at the
+ *     fixed-accuracy cut and truncation-error PSNR
+ *
+ *   - selection at equal PSNR (Alg.1 lines 7-10)
+ * DESIGN.md section 3 lists every reading taken where the paper is silent.
+ *
+ * Conventions
+ *   - dims are C order: dims[0] slowest, dims[ndims-1] fastest (contiguous).
+ *   - All entry points are extern "C", never throw, never abort; they return a
+ *     sel_status (0 = OK, < 0 = error) and leave *out untouched on error.
+ *   - A plan is not reentrant: at most one estimate call in flight per plan.
+ *     Distinct plans are independent.  The plan owns all device workspace.
+ *   - Device pointers must be CUDA device (or managed) memory of the current
+ *     device, float32, C-contiguous; 16-byte alignment enables the vector path
+ *     (torch's allocator guarantees 256 B).  The field must stay valid and
+ *     unmodified until the call returns.
+ *   - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Estimate calls enqueue on that stream and synchronise it before
+ *     returning the host-side result.
+ */
+#ifndef SEL_H
+#define SEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SEL_OK = 0,
+  SEL_EINVAL = -1,      /* bad argument: ndims not in {1,2,3}, dims < 1, prod(dims) overflow,
+                           eb not finite or <= 0, 1/(2 eb_abs) not finite in float, stride < 1,
+                           block != 4, NULL pointer, unknown option key */
+  SEL_ENOMEM = -2,      /* device or host allocation failed */
+  SEL_ECUDA = -3,       /* any CUDA runtime error; sel_strerror(SEL_ECUDA) has the message */
+  SEL_ENONFINITE = -4,  /* the field contains NaN or +-Inf (detected on the device) */
+  SEL_EDEGENERATE = -5, /* relative eb with VR == 0, or no SZ point besides the origin */
+  SEL_ENOTIMPL = -6
+} sel_status;
+
+typedef enum { SEL_EB_ABS = 0, SEL_EB_REL = 1 } sel_eb_mode;
+
+typedef struct sel_plan_st *sel_plan_t;
+
+/* Per-field result.  The first six members are north_star's result tuple. */
+typedef struct {
+  double sz_bits_per_value;  /* H + offset + 32*p_ovf  (bins of width 2*eb_abs)               */
+  double sz_psnr;            /* 20 log10(VR/eb_abs) + 10 log10 3              (Eq. psnr-sz)  */
+  double zfp_bits_per_value; /* exact fixed-accuracy EC bits / values in processed blocks     */
+  double zfp_psnr;           /* 20 log10 VR - 10 log10 MSE; +INF if MSE == 0                  */
+  int32_t choice;            /* Alg.1 selection bit s_i: 0 = SZ, 1 = ZFP                      */
+  int32_t matched;           /* 1 if compared at equal PSNR; 0 = fallback at the user's eb    */
+  /* diagnostics (parity tests compare these too) */
+  double value_range;        /* (double)max - (double)min over the whole field                */
+  double eb_abs;             /* absolute error bound used                                     */
+  double sz_entropy;         /* H in bits/value                                               */
+  double sz_overflow_frac;   /* fraction of SZ points in the overflow ("unpredictable") slot */
+  double sz_bits_matched;    /* BR_sz at the PSNR-matched bin delta* (Alg.1 line 9)          */
+  double sz_eb_matched;      /* delta_star / 2: SZ bound giving PSNR_zfp (Alg.1 line 11 reading) */
+  double zfp_mse;            /* sum_b E_b / n_values                                          */
+  uint64_t n_sz_points;      /* SZ residuals histogrammed (processed points minus the origin) */
+  uint64_t n_values;         /* real values in processed blocks                               */
+  uint64_t n_blocks;         /* processed 4^d blocks                                          */
+  uint64_t zfp_total_bits;   /* sum of per-block EC bits incl. headers                        */
+  double zfp_err_sum;        /* sum_b E_b                                                     */
+  int32_t minexp;            /* floor(log2 eb_abs)                                            */
+  float r_f;                 /* float(1/(2 eb_abs)), the quantiser scale                      */
+  int32_t status;            /* sel_status of this field (batch calls)                        */
+  int32_t reserved;
+} sel_result;
+
+/* Create a plan for fields of shape dims[0..ndims-1].
+ *   mode, eb : SEL_EB_ABS -> eb_abs = eb; SEL_EB_REL -> eb_abs = eb * VR (Alg.1 line 2)
+ *   stride   : ndims entries >= 1, block b is processed iff b_a % stride[a] == 0 for
+ *              every axis a; NULL = all 1 (every block)
+ *   block    : ZFP block edge, must be 4
+ * Allocates the device workspace on the current device.  Errors: SEL_EINVAL,
+ * SEL_ENOMEM, SEL_ECUDA. */
+int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double eb,
+             const int32_t *stride, int32_t block);
+
+/* Options: "sz_offset_bits" (default 0.5); "debug" (1 = dump intermediates
+ * for sel_debug_copy; test sizes only); "kernel_timing" (1 = record CUDA events
+ * around every launch, read with sel_kernel_times). Errors: SEL_EINVAL. */
+int sel_set_option(sel_plan_t plan, const char *key, double value);
+
+/* Estimate one field already in device memory (d_field: device, N floats).
+ * Enqueues value range -> fused SZ/ZFP pass -> finalize on `stream`, copies the
+ * result to pinned host memory, synchronises `stream`, fills *out.
+ * Errors: SEL_EINVAL, SEL_ENONFINITE, SEL_EDEGENERATE, SEL_ECUDA. */
+int sel_estimate(sel_plan_t plan, const float *d_field, void *stream, sel_result *out);
+
+/* Estimate n fields of the plan's shape (d_fields: HOST array of n DEVICE
+ * pointers).  out[i].status holds each field's status; returns SEL_OK if the
+ * launches succeeded (individual fields may still carry an error status). */
+int sel_estimate_batch(sel_plan_t plan, const float *const *d_fields, int n, void *stream,
+                       sel_result *out);
+
+/* End-to-end entry: fields in HOST memory (pinned for full speed).  The plan
+ * stages each field into device buffers with cudaMemcpyAsync on an internal
+ * copy stream, double-buffered so the copy of field i+1 overlaps the estimate
+ * of field i.  h_fields: host array of n host pointers. */
+int sel_estimate_batch_host(sel_plan_t plan, const float *const *h_fields, int n,
+                            void *stream, sel_result *out);
+
+/* Pure host: Alg.1 lines 7-10 recomputed from r's fields
+ * (sz_bits_per_value, zfp_bits_per_value, zfp_psnr, zfp_mse, value_range, eb_abs).
+ * Ties go to ZFP.  Errors: SEL_EINVAL (NULL). */
+int sel_choose(const sel_result *r, int32_t *choice);
+
+/* Test-only: copy a debug dump of the LAST sel_estimate (requires option debug=1):
+ *   "codes"  int32[N]           slot per point, -1 where no code was formed
+ *   "hist"   uint64[65536]
+ *   "emax"   int32[n_blocks]    -127 for an all-zero block
+ *   "coef"   int32[n_blocks*4^d] lifted coefficients, natural order
+ *   "uword"  uint32[n_blocks*4^d] negabinary words, sequency order
+ *   "bits"   uint32[n_blocks]
+ *   "err"    double[n_blocks]   E_b
+ * bytes must equal the array size.  Errors: SEL_EINVAL, SEL_ECUDA. */
+int sel_debug_copy(sel_plan_t plan, const char *what, void *host_dst, uint64_t bytes);
+
+/* Per-kernel device time accumulated since the last reset (option kernel_timing=1):
+ * ms[0] value range, ms[1] fused estimate, ms[2] finalize; launches[k] the count.
+ * reset != 0 clears the accumulators after reading. */
+int sel_kernel_times(sel_plan_t plan, double ms[3], uint64_t launches[3], int reset);
+
+/* Number of processed blocks / values and the device workspace size of a plan. */
+uint64_t sel_processed_blocks(sel_plan_t plan);
+uint64_t sel_processed_values(sel_plan_t plan);
+size_t sel_workspace_bytes(sel_plan_t plan);
+/* Total kernel launches issued by this plan so far. */
+uint64_t sel_launch_count(sel_plan_t plan);
+
+void sel_plan_destroy(sel_plan_t plan);
+
+/* Static description of a status; for SEL_ECUDA the last CUDA error message. */
+const char *sel_strerror(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEL_H */

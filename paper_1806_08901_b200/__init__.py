@@ -1,0 +1,246 @@
+"""B200-native SZ-vs-ZFP rate-distortion estimator (arXiv 1806.08901, Alg. 1 lines 1-10).
+
+Thin ctypes binding over the C ABI in ``include/sel.h`` (``libsel.so``, built in-tree by
+``paper_1806_08901_b200.build``).  This module only marshals arguments: every step of
+the estimate runs in the sm_100a kernels behind the ABI.  There is no CPU fallback --
+if ``libsel.so`` is missing or CUDA is unavailable, calls raise.
+
+PyTorch is used for device memory (``tensor.data_ptr()``) and streams
+(``torch.cuda.current_stream().cuda_stream``) only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsel.so")
+
+SEL_OK, SEL_EINVAL, SEL_ENOMEM, SEL_ECUDA, SEL_ENONFINITE, SEL_EDEGENERATE, SEL_ENOTIMPL = (
+    0, -1, -2, -3, -4, -5, -6)
+EB_ABS, EB_REL = 0, 1
+
+# every entry point declared in include/sel.h
+EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_batch",
+           "sel_estimate_batch_host", "sel_choose", "sel_debug_copy", "sel_kernel_times",
+           "sel_processed_blocks", "sel_processed_values", "sel_workspace_bytes",
+           "sel_launch_count", "sel_plan_destroy", "sel_strerror")
+
+
+class SelError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"sel status {status}: {msg}")
+        self.status = status
+
+
+class Result(C.Structure):
+    """Mirror of ``sel_result`` (include/sel.h)."""
+    _fields_ = [
+        ("sz_bits_per_value", C.c_double), ("sz_psnr", C.c_double),
+        ("zfp_bits_per_value", C.c_double), ("zfp_psnr", C.c_double),
+        ("choice", C.c_int32), ("matched", C.c_int32),
+        ("value_range", C.c_double), ("eb_abs", C.c_double), ("sz_entropy", C.c_double),
+        ("sz_overflow_frac", C.c_double), ("sz_bits_matched", C.c_double),
+        ("sz_eb_matched", C.c_double), ("zfp_mse", C.c_double),
+        ("n_sz_points", C.c_uint64), ("n_values", C.c_uint64), ("n_blocks", C.c_uint64),
+        ("zfp_total_bits", C.c_uint64), ("zfp_err_sum", C.c_double),
+        ("minexp", C.c_int32), ("r_f", C.c_float), ("status", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+_lib = None
+
+
+def lib():
+    """Load libsel.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_1806_08901_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.sel_plan.argtypes = [C.POINTER(P), C.c_int, P, C.c_int, C.c_double, P, C.c_int32]
+        L.sel_plan.restype = C.c_int
+        L.sel_set_option.argtypes = [P, C.c_char_p, C.c_double]
+        L.sel_set_option.restype = C.c_int
+        L.sel_estimate.argtypes = [P, P, P, C.POINTER(Result)]
+        L.sel_estimate.restype = C.c_int
+        L.sel_estimate_batch.argtypes = [P, P, C.c_int, P, P]
+        L.sel_estimate_batch.restype = C.c_int
+        L.sel_estimate_batch_host.argtypes = [P, P, C.c_int, P, P]
+        L.sel_estimate_batch_host.restype = C.c_int
+        L.sel_choose.argtypes = [C.POINTER(Result), C.POINTER(C.c_int32)]
+        L.sel_choose.restype = C.c_int
+        L.sel_debug_copy.argtypes = [P, C.c_char_p, P, C.c_uint64]
+        L.sel_debug_copy.restype = C.c_int
+        L.sel_kernel_times.argtypes = [P, P, P, C.c_int]
+        L.sel_kernel_times.restype = C.c_int
+        for f in ("sel_processed_blocks", "sel_processed_values", "sel_launch_count"):
+            getattr(L, f).argtypes = [P]
+            getattr(L, f).restype = C.c_uint64
+        L.sel_workspace_bytes.argtypes = [P]
+        L.sel_workspace_bytes.restype = C.c_size_t
+        L.sel_plan_destroy.argtypes = [P]
+        L.sel_plan_destroy.restype = None
+        L.sel_strerror.argtypes = [C.c_int]
+        L.sel_strerror.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def strerror(status: int) -> str:
+    return lib().sel_strerror(status).decode()
+
+
+def _check(status: int):
+    if status != SEL_OK:
+        raise SelError(status, strerror(status))
+
+
+def _stream_ptr(stream):
+    if stream is not None:
+        return C.c_void_p(int(stream))
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _device_ptr(t) -> int:
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor on a CUDA device")
+    if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+        raise ValueError("field must be a contiguous float32 CUDA tensor")
+    return t.data_ptr()
+
+
+def _host_ptr(a) -> int:
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous():
+                raise ValueError("host field must be a contiguous float32 CPU tensor")
+            return a.data_ptr()
+    except ImportError:  # pragma: no cover
+        pass
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous):
+        raise ValueError("host field must be a C-contiguous float32 array")
+    return a.ctypes.data
+
+
+class Plan:
+    """An estimation plan for fields of one shape (owns the device workspace)."""
+
+    def __init__(self, shape, eb: float, mode: str = "rel", stride=None, block: int = 4):
+        shape = tuple(int(s) for s in shape)
+        self.shape = shape
+        self.ndims = len(shape)
+        self.eb = float(eb)
+        self.mode = mode
+        self._dims = (C.c_int64 * max(self.ndims, 1))(*shape)
+        self._stride = None if stride is None else (C.c_int32 * self.ndims)(*[int(s) for s in stride])
+        self._h = C.c_void_p()
+        m = EB_REL if mode == "rel" else EB_ABS
+        if mode not in ("rel", "abs"):
+            raise ValueError("mode must be 'rel' or 'abs'")
+        _check(lib().sel_plan(C.byref(self._h), self.ndims, self._dims, m, self.eb,
+                              self._stride, int(block)))
+
+    # -- options / introspection
+    def set_option(self, key: str, value: float):
+        _check(lib().sel_set_option(self._h, key.encode(), float(value)))
+        return self
+
+    @property
+    def processed_blocks(self) -> int:
+        return int(lib().sel_processed_blocks(self._h))
+
+    @property
+    def processed_values(self) -> int:
+        return int(lib().sel_processed_values(self._h))
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(lib().sel_workspace_bytes(self._h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().sel_launch_count(self._h))
+
+    def kernel_times(self, reset: bool = False):
+        ms = (C.c_double * 3)()
+        n = (C.c_uint64 * 3)()
+        _check(lib().sel_kernel_times(self._h, ms, n, int(reset)))
+        return list(ms), list(n)
+
+    # -- estimates
+    def estimate(self, field, stream=None) -> dict:
+        r = Result()
+        _check(lib().sel_estimate(self._h, C.c_void_p(_device_ptr(field)), _stream_ptr(stream),
+                                  C.byref(r)))
+        return r.to_dict()
+
+    def estimate_batch(self, fields, stream=None) -> list[dict]:
+        n = len(fields)
+        ptrs = (C.c_void_p * n)(*[_device_ptr(f) for f in fields])
+        out = (Result * n)()
+        _check(lib().sel_estimate_batch(self._h, ptrs, n, _stream_ptr(stream), out))
+        return [o.to_dict() for o in out]
+
+    def estimate_batch_host(self, fields, stream=None) -> list[dict]:
+        n = len(fields)
+        ptrs = (C.c_void_p * n)(*[_host_ptr(f) for f in fields])
+        out = (Result * n)()
+        _check(lib().sel_estimate_batch_host(self._h, ptrs, n, _stream_ptr(stream), out))
+        return [o.to_dict() for o in out]
+
+    def debug_copy(self, what: str) -> np.ndarray:
+        S = 4 ** self.ndims
+        B = self.processed_blocks
+        spec = {"codes": (np.int32, self.shape), "hist": (np.uint64, (65536,)),
+                "emax": (np.int32, (B,)), "coef": (np.int32, (B, S)),
+                "uword": (np.uint32, (B, S)), "bits": (np.uint32, (B,)),
+                "err": (np.float64, (B,))}[what]
+        a = np.empty(spec[1], spec[0])
+        _check(lib().sel_debug_copy(self._h, what.encode(), a.ctypes.data_as(C.c_void_p), a.nbytes))
+        return a
+
+    def close(self):
+        if self._h:
+            lib().sel_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def estimate(field, eb: float, mode: str = "rel", stride=None, stream=None) -> dict:
+    """One-shot: SZ/ZFP rate-distortion estimate and Alg. 1 choice for a CUDA tensor."""
+    with Plan(tuple(field.shape), eb, mode, stride) as p:
+        return p.estimate(field, stream)
+
+
+def choose(result: dict) -> int:
+    """Host-side Alg. 1 lines 7-10 recomputed from a result dict."""
+    r = Result()
+    for k, _ in Result._fields_:
+        if k in result:
+            setattr(r, k, result[k])
+    c = C.c_int32()
+    _check(lib().sel_choose(C.byref(r), C.byref(c)))
+    return int(c.value)

@@ -1,0 +1,443 @@
+// sel_api.cu -- host runtime behind include/sel.h: plans own the device workspace,
+// launches are stream-ordered (K1 value range -> K2 fused estimate -> K3 finalize),
+// one small D2H of the result per call.  No CPU fallback: every estimate runs in
+// the kernels of sel_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sel_internal.h"
+
+using namespace sel;
+
+namespace {
+
+thread_local std::string g_cuda_msg = "no CUDA error recorded";
+
+int cuda_fail(cudaError_t e, const char *what) {
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  g_cuda_msg = buf;
+  return SEL_ECUDA;
+}
+
+#define CK(call)                                         \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+struct TimingSlot {
+  cudaEvent_t ev[4];   // before K1, after K1, after K2, after K3
+};
+
+}  // namespace
+
+struct sel_plan_st {
+  int device = 0;
+  int sm_count = 0;
+  Geo geo{};
+  int mode = 0;
+  double eb = 0.0;
+  double sz_offset = 0.5;
+  int debug = 0;
+  int timing = 0;
+  int mm_ctas = 0;
+  int est_ctas_cache[2][2] = {{0, 0}, {0, 0}};   // [vec][debug]
+  int est_ctas_cap = 0;
+  uint64_t n_sz = 0, n_values = 0;
+  int size = 0;                                   // 4^d
+
+  void *ws_mem = nullptr;
+  size_t ws_bytes = 0;
+  Workspace ws{};
+
+  sel_result *d_res = nullptr;
+  sel_result *h_res = nullptr;   // pinned
+  int res_cap = 0;
+
+  // debug dumps
+  void *dbg_mem = nullptr;
+  DebugPtrs dbg{};
+  unsigned long long *dbg_hist = nullptr;
+
+  // end-to-end staging
+  float *d_stage[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+
+  // kernel timing
+  std::vector<TimingSlot> tslots;
+  double ms[3] = {0, 0, 0};
+  uint64_t tcount[3] = {0, 0, 0};
+
+  uint64_t launches = 0;
+};
+
+namespace {
+
+int est_ctas(sel_plan_t p, int vec, int dbg) {
+  int &c = p->est_ctas_cache[vec][dbg];
+  if (c == 0) {
+    Geo g = p->geo;
+    g.vec = vec;
+    c = estimate_max_ctas(g, dbg, p->sm_count);
+    if (c < 0) { c = 0; return -1; }
+    if (c > p->est_ctas_cap) c = p->est_ctas_cap;
+  }
+  return c;
+}
+
+int ensure_results(sel_plan_t p, int n) {
+  if (n <= p->res_cap) return SEL_OK;
+  if (p->d_res) cudaFree(p->d_res);
+  if (p->h_res) cudaFreeHost(p->h_res);
+  p->d_res = nullptr;
+  p->h_res = nullptr;
+  p->res_cap = 0;
+  CK(cudaMalloc(&p->d_res, sizeof(sel_result) * (size_t)n));
+  CK(cudaMallocHost(&p->h_res, sizeof(sel_result) * (size_t)n));
+  p->res_cap = n;
+  return SEL_OK;
+}
+
+int ensure_timing(sel_plan_t p, int n) {
+  while ((int)p->tslots.size() < n) {
+    TimingSlot s;
+    for (auto &e : s.ev) CK(cudaEventCreate(&e));
+    p->tslots.push_back(s);
+  }
+  return SEL_OK;
+}
+
+int ensure_debug(sel_plan_t p) {
+  if (p->dbg_mem) return SEL_OK;
+  const size_t N = (size_t)p->geo.N, B = (size_t)p->geo.n_pb, S = (size_t)p->size;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+  size_t o_codes = take(N * 4), o_emax = take(B * 4), o_coef = take(B * S * 4),
+         o_uw = take(B * S * 4), o_bits = take(B * 4), o_err = take(B * 8),
+         o_hist = take((size_t)kNSlots * 8);
+  void *m = nullptr;
+  if (cudaMalloc(&m, off) != cudaSuccess) return SEL_ENOMEM;
+  char *b = (char *)m;
+  p->dbg_mem = m;
+  p->dbg.codes = (int32_t *)(b + o_codes);
+  p->dbg.emax = (int32_t *)(b + o_emax);
+  p->dbg.coef = (int32_t *)(b + o_coef);
+  p->dbg.uword = (uint32_t *)(b + o_uw);
+  p->dbg.bits = (uint32_t *)(b + o_bits);
+  p->dbg.err = (double *)(b + o_err);
+  p->dbg_hist = (unsigned long long *)(b + o_hist);
+  return SEL_OK;
+}
+
+// Enqueue K1 -> K2 -> K3 for one field; result lands in d_out.
+int enqueue_field(sel_plan_t p, const float *x, cudaStream_t st, sel_result *d_out, int slot) {
+  const int vec = (p->geo.n[2] % 4 == 0) && (((uintptr_t)x & 15u) == 0);
+  const int dbg = p->debug ? 1 : 0;
+  const int ctas = est_ctas(p, vec, dbg);
+  if (ctas <= 0) return cuda_fail(cudaGetLastError(), "occupancy query");
+  Geo g = p->geo;
+  g.vec = vec;
+  if (dbg) CK(cudaMemsetAsync(p->dbg.codes, 0xff, (size_t)p->geo.N * 4, st));
+  TimingSlot *ts = p->timing ? &p->tslots[slot] : nullptr;
+  if (ts) CK(cudaEventRecord(ts->ev[0], st));
+  int rc = launch_minmax(x, g.N, p->mm_ctas, p->ws, p->mode, p->eb, st);
+  if (rc) return cuda_fail(cudaGetLastError(), "k_minmax launch");
+  if (ts) CK(cudaEventRecord(ts->ev[1], st));
+  rc = launch_estimate(x, g, ctas, p->ws, dbg ? &p->dbg : nullptr, st);
+  if (rc) return cuda_fail(cudaGetLastError(), "k_estimate launch");
+  if (ts) CK(cudaEventRecord(ts->ev[2], st));
+  FinalizeArgs fa;
+  fa.mode = p->mode;
+  fa.eb = p->eb;
+  fa.sz_offset = p->sz_offset;
+  fa.n_sz = p->n_sz;
+  fa.n_values = p->n_values;
+  fa.n_blocks = (uint64_t)p->geo.n_pb;
+  fa.est_ctas = ctas;
+  rc = launch_finalize(p->ws, fa, d_out, dbg ? p->dbg_hist : nullptr, st);
+  if (rc) return cuda_fail(cudaGetLastError(), "k_finalize launch");
+  if (ts) CK(cudaEventRecord(ts->ev[3], st));
+  p->launches += 3;
+  return SEL_OK;
+}
+
+int collect_timing(sel_plan_t p, int n) {
+  if (!p->timing) return SEL_OK;
+  for (int f = 0; f < n; ++f) {
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, p->tslots[f].ev[k], p->tslots[f].ev[k + 1]));
+      p->ms[k] += ms;
+      p->tcount[k] += 1;
+    }
+  }
+  return SEL_OK;
+}
+
+int finish(sel_plan_t p, cudaStream_t st, int n, sel_result *out) {
+  CK(cudaMemcpyAsync(p->h_res, p->d_res, sizeof(sel_result) * (size_t)n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int rc = collect_timing(p, n);
+  if (rc) return rc;
+  memcpy(out, p->h_res, sizeof(sel_result) * (size_t)n);
+  return SEL_OK;
+}
+
+uint64_t real_in_processed(int64_t n, int64_t s) {
+  // sum over processed blocks b (b % s == 0) of the real values min(4, n - 4b)
+  uint64_t r = 0;
+  const int64_t nb = (n + 3) / 4;
+  for (int64_t b = 0; b < nb; b += s) r += (uint64_t)((n - 4 * b) < 4 ? (n - 4 * b) : 4);
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sel_strerror(int status) {
+  switch (status) {
+    case SEL_OK: return "ok";
+    case SEL_EINVAL: return "invalid argument";
+    case SEL_ENOMEM: return "out of memory";
+    case SEL_ECUDA: return g_cuda_msg.c_str();
+    case SEL_ENONFINITE: return "field contains NaN or Inf";
+    case SEL_EDEGENERATE: return "degenerate field (relative bound with zero value range, or no SZ point)";
+    case SEL_ENOTIMPL: return "not implemented";
+    default: return "unknown status";
+  }
+}
+
+int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double eb,
+             const int32_t *stride, int32_t block) {
+  if (!out || !dims || ndims < 1 || ndims > 3) return SEL_EINVAL;
+  if (block != 4) return SEL_EINVAL;
+  if (mode != SEL_EB_ABS && mode != SEL_EB_REL) return SEL_EINVAL;
+  if (!std::isfinite(eb) || !(eb > 0.0)) return SEL_EINVAL;
+  if (mode == SEL_EB_ABS && !std::isfinite((float)(1.0 / (2.0 * eb)))) return SEL_EINVAL;
+  Geo g{};
+  for (int a = 0; a < 3; ++a) { g.n[a] = 1; g.s[a] = 1; }
+  int64_t N = 1;
+  for (int a = 0; a < ndims; ++a) {
+    const int ax = 3 - ndims + a;
+    if (dims[a] < 1) return SEL_EINVAL;
+    if (N > INT64_MAX / 4 / dims[a]) return SEL_EINVAL;
+    N *= dims[a];
+    g.n[ax] = dims[a];
+    if (stride) {
+      if (stride[a] < 1) return SEL_EINVAL;
+      g.s[ax] = stride[a];
+    }
+  }
+  g.N = N;
+  g.ndims = ndims;
+  g.n_pb = 1;
+  uint64_t nv = 1;
+  for (int a = 0; a < 3; ++a) {
+    g.nb[a] = (g.n[a] + 3) / 4;
+    g.npb[a] = (g.nb[a] + g.s[a] - 1) / g.s[a];
+    g.n_pb *= g.npb[a];
+    nv *= real_in_processed(g.n[a], g.s[a]);
+  }
+  // the 3-axis view pads missing leading axes with extent 1: they contribute
+  // real_in_processed(1, 1) = 1 value, as they should.
+  auto *p = new (std::nothrow) sel_plan_st();
+  if (!p) return SEL_ENOMEM;
+  p->geo = g;
+  p->mode = mode;
+  p->eb = eb;
+  p->size = ndims == 1 ? 4 : (ndims == 2 ? 16 : 64);
+  p->n_values = nv;
+  p->n_sz = nv - 1;   // the field origin is always in a processed block
+  if (cudaGetDevice(&p->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
+    cuda_fail(cudaGetLastError(), "cudaGetDevice");
+    delete p;
+    return SEL_ECUDA;
+  }
+  p->mm_ctas = minmax_ctas(N, p->sm_count);
+  p->est_ctas_cap = 8 * p->sm_count;
+  // workspace layout
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+  const size_t o_hist = take((size_t)kNSlots * 8), o_mmp = take((size_t)p->mm_ctas * sizeof(float2)),
+               o_mmf = take((size_t)p->mm_ctas * 4), o_prm = take(sizeof(Params)),
+               o_ep = take((size_t)p->est_ctas_cap * sizeof(Partial)),
+               o_fp = take((size_t)kFinCTAs * 8), o_fo = take(8), o_tk = take(2 * 4);
+  if (cudaMalloc(&p->ws_mem, off) != cudaSuccess) {
+    cudaGetLastError();
+    delete p;
+    return SEL_ENOMEM;
+  }
+  p->ws_bytes = off;
+  char *b = (char *)p->ws_mem;
+  p->ws.hist = (unsigned long long *)(b + o_hist);
+  p->ws.mm_part = (float2 *)(b + o_mmp);
+  p->ws.mm_flag = (int32_t *)(b + o_mmf);
+  p->ws.params = (Params *)(b + o_prm);
+  p->ws.est_part = (Partial *)(b + o_ep);
+  p->ws.fin_part = (double *)(b + o_fp);
+  p->ws.fin_ovf = (unsigned long long *)(b + o_fo);
+  p->ws.tickets = (unsigned int *)(b + o_tk);
+  if (cudaMemset(p->ws_mem, 0, off) != cudaSuccess || ensure_results(p, 1) != SEL_OK) {
+    cuda_fail(cudaGetLastError(), "workspace init");
+    sel_plan_destroy(p);
+    return SEL_ECUDA;
+  }
+  *out = p;
+  return SEL_OK;
+}
+
+int sel_set_option(sel_plan_t p, const char *key, double value) {
+  if (!p || !key) return SEL_EINVAL;
+  if (!strcmp(key, "sz_offset_bits")) {
+    if (!std::isfinite(value)) return SEL_EINVAL;
+    p->sz_offset = value;
+    return SEL_OK;
+  }
+  if (!strcmp(key, "debug")) {
+    p->debug = value != 0.0;
+    if (p->debug) return ensure_debug(p);
+    return SEL_OK;
+  }
+  if (!strcmp(key, "kernel_timing")) {
+    p->timing = value != 0.0;
+    return SEL_OK;
+  }
+  return SEL_EINVAL;
+}
+
+int sel_estimate(sel_plan_t p, const float *d_field, void *stream, sel_result *out) {
+  if (!p || !d_field || !out) return SEL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_results(p, 1);
+  if (rc) return rc;
+  if (p->timing && (rc = ensure_timing(p, 1))) return rc;
+  if ((rc = enqueue_field(p, d_field, st, p->d_res, 0))) return rc;
+  sel_result r;
+  if ((rc = finish(p, st, 1, &r))) return rc;
+  if (r.status != SEL_OK) return r.status;
+  *out = r;
+  return SEL_OK;
+}
+
+int sel_estimate_batch(sel_plan_t p, const float *const *d_fields, int n, void *stream,
+                       sel_result *out) {
+  if (!p || !d_fields || !out || n < 0) return SEL_EINVAL;
+  if (n == 0) return SEL_OK;
+  for (int f = 0; f < n; ++f) if (!d_fields[f]) return SEL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_results(p, n);
+  if (rc) return rc;
+  if (p->timing && (rc = ensure_timing(p, n))) return rc;
+  for (int f = 0; f < n; ++f)
+    if ((rc = enqueue_field(p, d_fields[f], st, p->d_res + f, f))) return rc;
+  return finish(p, st, n, out);
+}
+
+int sel_estimate_batch_host(sel_plan_t p, const float *const *h_fields, int n, void *stream,
+                            sel_result *out) {
+  if (!p || !h_fields || !out || n < 0) return SEL_EINVAL;
+  if (n == 0) return SEL_OK;
+  for (int f = 0; f < n; ++f) if (!h_fields[f]) return SEL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_results(p, n);
+  if (rc) return rc;
+  if (p->timing && (rc = ensure_timing(p, n))) return rc;
+  const size_t bytes = (size_t)p->geo.N * sizeof(float);
+  if (!p->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&p->ev_copied[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&p->ev_done[b], cudaEventDisableTiming));
+    }
+  }
+  for (int b = 0; b < 2; ++b)
+    if (!p->d_stage[b] && cudaMalloc(&p->d_stage[b], bytes) != cudaSuccess) return SEL_ENOMEM;
+  // double-buffered: copy of field f+1 (copy stream) overlaps the estimate of f
+  for (int f = 0; f < n; ++f) {
+    const int b = f & 1;
+    if (f >= 2) CK(cudaStreamWaitEvent(p->copy_stream, p->ev_done[b], 0));
+    CK(cudaMemcpyAsync(p->d_stage[b], h_fields[f], bytes, cudaMemcpyHostToDevice, p->copy_stream));
+    CK(cudaEventRecord(p->ev_copied[b], p->copy_stream));
+    CK(cudaStreamWaitEvent(st, p->ev_copied[b], 0));
+    if ((rc = enqueue_field(p, p->d_stage[b], st, p->d_res + f, f))) return rc;
+    CK(cudaEventRecord(p->ev_done[b], st));
+  }
+  return finish(p, st, n, out);
+}
+
+int sel_choose(const sel_result *r, int32_t *choice) {
+  if (!r || !choice) return SEL_EINVAL;
+  const double vr = r->value_range, eb = r->eb_abs, mse = r->zfp_mse;
+  const double bsz = r->sz_bits_per_value, bzfp = r->zfp_bits_per_value, pz = r->zfp_psnr;
+  if (!(mse > 0.0) || !(vr > 0.0) || !std::isfinite(pz)) {
+    *choice = bsz < bzfp ? 0 : 1;
+    return SEL_OK;
+  }
+  const double delta = vr * std::sqrt(12.0) * std::pow(10.0, -pz / 20.0);
+  double bm = bsz + std::log2(2.0 * eb / delta);
+  if (bm < 0.0) bm = 0.0;
+  *choice = bm < bzfp ? 0 : 1;
+  return SEL_OK;
+}
+
+int sel_debug_copy(sel_plan_t p, const char *what, void *dst, uint64_t bytes) {
+  if (!p || !what || !dst || !p->dbg_mem) return SEL_EINVAL;
+  const uint64_t N = (uint64_t)p->geo.N, B = (uint64_t)p->geo.n_pb, S = (uint64_t)p->size;
+  const void *src = nullptr;
+  uint64_t need = 0;
+  if (!strcmp(what, "codes")) { src = p->dbg.codes; need = N * 4; }
+  else if (!strcmp(what, "hist")) { src = p->dbg_hist; need = (uint64_t)kNSlots * 8; }
+  else if (!strcmp(what, "emax")) { src = p->dbg.emax; need = B * 4; }
+  else if (!strcmp(what, "coef")) { src = p->dbg.coef; need = B * S * 4; }
+  else if (!strcmp(what, "uword")) { src = p->dbg.uword; need = B * S * 4; }
+  else if (!strcmp(what, "bits")) { src = p->dbg.bits; need = B * 4; }
+  else if (!strcmp(what, "err")) { src = p->dbg.err; need = B * 8; }
+  else return SEL_EINVAL;
+  if (bytes != need) return SEL_EINVAL;
+  CK(cudaMemcpy(dst, src, need, cudaMemcpyDeviceToHost));
+  return SEL_OK;
+}
+
+int sel_kernel_times(sel_plan_t p, double ms[3], uint64_t launches[3], int reset) {
+  if (!p || !ms || !launches) return SEL_EINVAL;
+  for (int k = 0; k < 3; ++k) { ms[k] = p->ms[k]; launches[k] = p->tcount[k]; }
+  if (reset) for (int k = 0; k < 3; ++k) { p->ms[k] = 0; p->tcount[k] = 0; }
+  return SEL_OK;
+}
+
+uint64_t sel_processed_blocks(sel_plan_t p) { return p ? (uint64_t)p->geo.n_pb : 0; }
+uint64_t sel_processed_values(sel_plan_t p) { return p ? p->n_values : 0; }
+size_t sel_workspace_bytes(sel_plan_t p) { return p ? p->ws_bytes : 0; }
+uint64_t sel_launch_count(sel_plan_t p) { return p ? p->launches : 0; }
+
+void sel_plan_destroy(sel_plan_t p) {
+  if (!p) return;
+  if (p->copy_stream) cudaStreamSynchronize(p->copy_stream);
+  if (p->ws_mem) cudaFree(p->ws_mem);
+  if (p->d_res) cudaFree(p->d_res);
+  if (p->h_res) cudaFreeHost(p->h_res);
+  if (p->dbg_mem) cudaFree(p->dbg_mem);
+  for (int b = 0; b < 2; ++b) {
+    if (p->d_stage[b]) cudaFree(p->d_stage[b]);
+    if (p->ev_copied[b]) cudaEventDestroy(p->ev_copied[b]);
+    if (p->ev_done[b]) cudaEventDestroy(p->ev_done[b]);
+  }
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  for (auto &s : p->tslots)
+    for (auto &e : s.ev) cudaEventDestroy(e);
+  delete p;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// sel_internal.h -- structures shared by the host runtime (sel_api.cu) and the
+// sm_100a kernels (sel_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+
+#include "../../include/sel.h"
+
+namespace sel {
+
+constexpr int kNSlots = 65536;       // 65,535 code bins + overflow slot
+constexpr int kOvfSlot = 65535;
+constexpr int kCenter = 32767;       // slot of code 0
+constexpr int kWinHalf = 8192;       // smem-privatised window: slots [kCenter-kWinHalf, kCenter+kWinHalf)
+constexpr int kWinBins = 2 * kWinHalf;
+constexpr int kFinCTAs = 64;         // finalize: 64 CTAs x 1024 slots
+constexpr int kFinThreads = 256;
+
+// Geometry, padded to 3 axes: axis 0 slowest.  For ndims < 3 the leading axes
+// have n = nb = npb = s = 1.
+struct Geo {
+  int64_t n[3];     // field extents
+  int64_t nb[3];    // blocks per axis = ceil(n/4)
+  int64_t npb[3];   // processed blocks per axis = ceil(nb/s)
+  int32_t s[3];     // sampling stride in blocks
+  int64_t n_pb;     // total processed blocks
+  int64_t N;        // total values
+  int32_t ndims;
+  int32_t vec;      // 1: fastest extent % 4 == 0 and field 16B-aligned -> float4 loads
+};
+
+// Derived per-field scalars written by the value-range kernel (Alg.1 line 2).
+struct Params {
+  float vmin, vmax;
+  double vr;
+  double eb_abs;
+  float r_f;
+  int32_t minexp;
+  int32_t status;   // sel_status
+  int32_t pad;
+};
+
+// Per-CTA partials of the fused pass.
+struct Partial {
+  uint64_t bits;    // sum of per-block EC bits
+  double err;       // sum of E_b
+};
+
+// Debug dump pointers (device), all may be null.
+struct DebugPtrs {
+  int32_t *codes;
+  int32_t *emax;
+  int32_t *coef;
+  uint32_t *uword;
+  uint32_t *bits;
+  double *err;
+};
+
+struct Workspace {
+  unsigned long long *hist;   // [kNSlots] u64
+  float2 *mm_part;            // [mm_ctas] (min,max)
+  int32_t *mm_flag;           // [mm_ctas] nonfinite flags
+  Params *params;             // [1]
+  Partial *est_part;          // [est_ctas]
+  double *fin_part;           // [kFinCTAs]
+  unsigned long long *fin_ovf;// [1]
+  unsigned int *tickets;      // [2] last-block-done counters (minmax, finalize)
+};
+
+struct FinalizeArgs {
+  int32_t mode;             // SEL_EB_ABS / SEL_EB_REL
+  double eb;
+  double sz_offset;
+  uint64_t n_sz;            // SZ points (host geometry)
+  uint64_t n_values;        // N_P
+  uint64_t n_blocks;
+  int32_t est_ctas;
+};
+
+// launchers (sel_kernels.cu)
+int launch_minmax(const float *x, int64_t N, int ctas, const Workspace &ws, int mode, double eb,
+                  cudaStream_t st);
+int launch_estimate(const float *x, const Geo &g, int ctas, const Workspace &ws,
+                    const DebugPtrs *dbg, cudaStream_t st);
+int launch_finalize(const Workspace &ws, const FinalizeArgs &fa, sel_result *d_out,
+                    unsigned long long *dbg_hist, cudaStream_t st);
+int estimate_max_ctas(const Geo &g, int debug, int sm_count);
+int minmax_ctas(int64_t N, int sm_count);
+
+}  // namespace sel

@@ -1,0 +1,324 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): bit-exact quantisation codes, histograms, block
+exponents, lifted int32 coefficients, negabinary words and per-block bit counts;
+entropy, bit-rates and PSNRs within 1e-6 relative; choices 100% equal.
+Inputs are the seeded synthetic generators in synth/ (DESIGN.md section 4).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+REL = 1e-6
+EXACT_KEYS = ("n_sz_points", "n_values", "n_blocks", "zfp_total_bits", "minexp", "r_f",
+              "choice", "matched", "value_range", "eb_abs")
+CLOSE_KEYS = ("sz_entropy", "sz_bits_per_value", "sz_psnr", "zfp_bits_per_value", "zfp_psnr",
+              "zfp_mse", "zfp_err_sum", "sz_bits_matched", "sz_eb_matched", "sz_overflow_frac")
+
+
+@pytest.fixture(scope="module")
+def sel():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_1806_08901_b200 import build
+    build.build()
+    import paper_1806_08901_b200 as sel
+    return sel
+
+
+def close(a, b, rel=REL, abs_=1e-12):
+    if isinstance(a, float) and (math.isinf(a) or math.isinf(b)):
+        return a == b
+    return abs(a - b) <= max(rel * max(abs(a), abs(b)), abs_)
+
+
+def compare_scalars(g, o, tag=""):
+    for k in EXACT_KEYS:
+        assert g[k] == o[k], (tag, k, g[k], o[k])
+    for k in CLOSE_KEYS:
+        assert close(float(g[k]), float(o[k])), (tag, k, g[k], o[k])
+    assert g["status"] == 0
+
+
+def run_gpu(sel, x, eb, mode="rel", stride=None, debug=False, offset_elems=0):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    if offset_elems:
+        buf = torch.empty(x.size + offset_elems, dtype=torch.float32, device="cuda")
+        buf[offset_elems:] = t.reshape(-1)
+        t = buf[offset_elems:].view(x.shape)
+    with sel.Plan(x.shape, eb, mode, stride) as p:
+        if debug:
+            p.set_option("debug", 1)
+        r = p.estimate(t)
+        dbg = {k: p.debug_copy(k) for k in ("codes", "hist", "emax", "coef", "uword", "bits", "err")} \
+            if debug else None
+    return r, dbg
+
+
+def check_case(sel, orc, x, eb, mode="rel", stride=None, offset_elems=0, tag=""):
+    o = orc.estimate(x, eb, mode=mode, stride=stride, debug=True)
+    g, gd = run_gpu(sel, x, eb, mode, stride, debug=True, offset_elems=offset_elems)
+    compare_scalars(g, o, tag)
+    od = o["debug"]
+    for k in ("codes", "hist", "emax", "coef", "uword", "bits"):
+        assert np.array_equal(gd[k].reshape(od[k].shape), od[k]), (tag, k)
+    assert np.allclose(gd["err"], od["err"], rtol=1e-12, atol=0), tag
+    # the non-debug instantiation (the one bench.py times) gives the same result
+    g2, _ = run_gpu(sel, x, eb, mode, stride, debug=False, offset_elems=offset_elems)
+    compare_scalars(g2, o, tag + "/nodebug")
+    for k in g:
+        if isinstance(g[k], float) and math.isnan(g[k]):
+            continue
+        assert g2[k] == g[k], (tag, k)          # deterministic run to run
+    # host-side Alg. 1 recomputation agrees with the device's choice
+    assert sel.choose(g) == g["choice"]
+    return g, o
+
+
+# ---------------------------------------------------------------- configs (small)
+def test_config1_exact(sel, orc):
+    import synth
+    x = synth.c1_field()
+    check_case(sel, orc, x, 1e-4, tag="C1")
+
+
+@pytest.mark.parametrize("i", [0, 1, 3])
+@pytest.mark.parametrize("stride", [None, (1, 10), (3, 2)])
+def test_config2_recipe_ragged(sel, orc, i, stride):
+    import synth
+    x = synth.c2_field(i, shape=(203, 517))          # ragged: neither dim % 4 == 0
+    check_case(sel, orc, x, 1e-4, stride=stride, tag=f"C2r{i}{stride}")
+
+
+@pytest.mark.parametrize("i", [0, 2, 3, 5, 9])
+@pytest.mark.parametrize("eb", [1e-3, 1e-4, 1e-5])
+def test_config3_recipe_ragged(sel, orc, i, eb):
+    import synth
+    x = synth.c3_field(i, shape=(37, 45, 70))
+    check_case(sel, orc, x, eb, tag=f"C3r{i}/{eb}")
+
+
+@pytest.mark.parametrize("i", [0, 1, 4])
+@pytest.mark.parametrize("stride", [None, (4, 4, 4), (1, 2, 3)])
+def test_config4_recipe(sel, orc, i, stride):
+    import synth
+    x = synth.c4_field(i, shape=(64, 64, 64))
+    check_case(sel, orc, x, 1e-4, stride=stride, tag=f"C4s{i}{stride}")
+
+
+@pytest.mark.parametrize("mix", [0, 1, 2])
+@pytest.mark.parametrize("eb", [1e-2, 1e-3, 1e-4, 1e-5, 1e-6, 1e-7])
+def test_config5_recipe(sel, orc, mix, eb):
+    import synth
+    x = synth.c5_field(mix, shape=(32, 48, 64))
+    g, o = check_case(sel, orc, x, eb, tag=f"C5s{mix}/{eb}")
+    if mix == 2 and eb <= 1e-6:
+        assert o["sz_overflow_frac"] > 0.5          # the histogram-width stress really is hit
+
+
+# ---------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("shape", [(100003,), (5,), (2, 3), (1, 1, 5), (3, 1, 9), (1, 700), (9, 10, 1)])
+def test_odd_shapes(sel, orc, shape):
+    rng = np.random.default_rng(len(shape) * 100 + shape[-1])
+    x = np.cumsum(rng.standard_normal(int(np.prod(shape)))).reshape(shape).astype(np.float32)
+    check_case(sel, orc, x, 1e-3, tag=f"odd{shape}")
+    check_case(sel, orc, x, 0.01, mode="abs", tag=f"odd{shape}abs")
+
+
+def test_misaligned_pointer_scalar_path(sel, orc):
+    import synth
+    x = synth.c2_field(4, shape=(64, 96))
+    check_case(sel, orc, x, 1e-4, offset_elems=1, tag="misaligned")
+
+
+def test_constant_and_zero_fields(sel, orc):
+    for x in (np.full((17, 23), 2.5, np.float32), np.zeros((8, 8, 8), np.float32),
+              np.full((40,), -1e-41, np.float32)):
+        g, o = check_case(sel, orc, x, 1e-3, mode="abs", tag=f"const{x.shape}")
+        assert g["sz_entropy"] == 0.0
+    with pytest.raises(sel.SelError) as e:
+        run_gpu(sel, np.full((8, 8), 1.0, np.float32), 1e-3, "rel")
+    assert e.value.status == sel.SEL_EDEGENERATE
+
+
+def test_nonfinite_rejected(sel):
+    for bad in (np.nan, np.inf, -np.inf):
+        x = np.ones((13, 9), np.float32)
+        x[7, 3] = bad
+        with pytest.raises(sel.SelError) as e:
+            run_gpu(sel, x, 1e-3)
+        assert e.value.status == sel.SEL_ENONFINITE
+
+
+def test_single_value_degenerate(sel):
+    with pytest.raises(sel.SelError) as e:
+        run_gpu(sel, np.ones((1,), np.float32), 1e-3, "abs")
+    assert e.value.status == sel.SEL_EDEGENERATE
+
+
+def test_extreme_values(sel, orc):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((24, 28, 32)).astype(np.float32)
+    x[:4, :4, :4] *= np.float32(1e-39)                   # subnormal block (emax clamp)
+    x[4:8, :4, :4] = np.float32(3.0e38) * np.sign(x[4:8, :4, :4])   # near FLT_MAX
+    x[8:12, 4:8, :] = 0.0                                 # empty blocks
+    x[12:, :, :] *= (rng.random((12, 28, 32)) < 0.7)      # 30% zeros
+    check_case(sel, orc, x, 1e-3, mode="abs", tag="extreme-abs")
+    check_case(sel, orc, x, 1e-6, mode="rel", tag="extreme-rel")
+    y = (rng.standard_normal((16, 16)) * 1e-30).astype(np.float32)   # BFP two-step scale path
+    check_case(sel, orc, y, 1e-3, tag="tiny")
+
+
+def test_offset_option(sel, orc):
+    import synth
+    x = synth.c1_field((64, 64), seed=4)
+    o = orc.estimate(x, 1e-4, sz_offset=0.0)
+    t = torch.from_numpy(x).cuda()
+    with sel.Plan(x.shape, 1e-4) as p:
+        p.set_option("sz_offset_bits", 0.0)
+        g = p.estimate(t)
+    compare_scalars(g, o, "offset0")
+
+
+# ---------------------------------------------------------------- batch APIs
+def test_batch_and_host_batch(sel, orc):
+    import synth
+    shape = (60, 90)
+    xs = [synth.c2_field(i, shape=shape) for i in range(5)]
+    ts = [torch.from_numpy(x).cuda() for x in xs]
+    hs = [torch.from_numpy(x).pin_memory() for x in xs]
+    with sel.Plan(shape, 1e-4) as p:
+        single = [p.estimate(t) for t in ts]
+        batch = p.estimate_batch(ts)
+        host = p.estimate_batch_host(hs)
+        host_np = p.estimate_batch_host(xs)
+        assert p.launch_count == 3 * (5 + 5 + 5 + 5)
+    for i, x in enumerate(xs):
+        o = orc.estimate(x, 1e-4)
+        for r in (single[i], batch[i], host[i], host_np[i]):
+            compare_scalars(r, o, f"batch{i}")
+
+
+def test_batch_reports_per_field_status(sel):
+    ts = [torch.ones(8, 8, device="cuda"), torch.arange(64, dtype=torch.float32, device="cuda").view(8, 8)]
+    with sel.Plan((8, 8), 1e-3) as p:
+        out = p.estimate_batch(ts)
+    assert out[0]["status"] == sel.SEL_EDEGENERATE and out[1]["status"] == 0
+
+
+def test_kernel_timing_option(sel):
+    t = torch.randn(256, 256, device="cuda")
+    with sel.Plan(t.shape, 1e-4) as p:
+        p.set_option("kernel_timing", 1)
+        for _ in range(3):
+            p.estimate(t)
+        ms, n = p.kernel_times(reset=True)
+    assert n == [3, 3, 3] and all(m > 0 for m in ms)
+
+
+# ---------------------------------------------------------------- full sizes
+def _padded_block(x, b, nd):
+    sl = []
+    for a in range(nd):
+        idx = np.minimum(np.arange(4 * b[a], 4 * b[a] + 4), x.shape[a] - 1)
+        sl.append(idx)
+    return x[np.ix_(*sl)].reshape(-1)
+
+
+def _sampled_block_check(orc, x, g, dbg, stride, nblocks=400, seed=0):
+    """Per-block parity on sampled processed blocks, computed one by one with
+    the oracle's step functions (full-size fields, BASELINE 'sampled outputs')."""
+    nd = x.ndim
+    nb = [(n + 3) // 4 for n in x.shape]
+    npb = [(nb[a] + stride[a] - 1) // stride[a] for a in range(nd)]
+    rng = np.random.default_rng(seed)
+    perm = orc.sequency_perm(nd)
+    r_f = np.float32(g["r_f"])
+    for _ in range(nblocks):
+        t = int(rng.integers(0, int(np.prod(npb))))
+        pc = np.unravel_index(t, npb)
+        b = [int(pc[a]) * stride[a] for a in range(nd)]
+        blk = _padded_block(x, b, nd)
+        e = orc.block_emax(blk)
+        assert dbg["emax"][t] == e
+        if e == -127:
+            assert dbg["bits"][t] == 1
+            continue
+        coef = orc.fwd_xform(orc.block_bfp(blk, e), nd)
+        assert np.array_equal(dbg["coef"][t], coef)
+        u = np.array([orc.negabinary(int(coef[p])) for p in perm], np.uint32)
+        assert np.array_equal(dbg["uword"][t], u)
+        p = orc.precision(e, g["minexp"], nd)
+        bits = 1 if p == 0 else 9 + orc.gt_count(u, 32 - p)
+        assert dbg["bits"][t] == bits
+        assert close(float(dbg["err"][t]), orc.block_err(coef, u, nd, 32 - p, e), rel=1e-12, abs_=0.0)
+        # SZ codes of the block's real points
+        for n in range(4 ** nd):
+            idx = tuple(4 * b[a] + (n // 4 ** (nd - 1 - a)) % 4 for a in range(nd))
+            if any(idx[a] >= x.shape[a] for a in range(nd)):
+                continue
+            if not any(idx):
+                assert dbg["codes"][idx] == -1
+                continue
+            assert dbg["codes"][idx] == orc.quantize(orc.lorenzo(x, idx), r_f), idx
+
+
+def _full_size_check(sel, orc, x, eb, stride=None, full_oracle=True, tag=""):
+    nd = x.ndim
+    st = stride or (1,) * nd
+    t = torch.from_numpy(x).cuda()
+    with sel.Plan(x.shape, eb, "rel", stride) as p:
+        g = p.estimate(t)                                 # bench launch configuration
+        p.set_option("debug", 1)
+        gd = p.estimate(t)
+        dbg = {k: p.debug_copy(k) for k in ("codes", "hist", "emax", "coef", "uword", "bits", "err")}
+    for k in g:
+        assert g[k] == gd[k] or (isinstance(g[k], float) and math.isnan(g[k])), (tag, k)
+    # properties at any size
+    assert int(dbg["hist"].sum()) == g["n_sz_points"]
+    assert int(dbg["bits"].astype(np.uint64).sum()) == g["zfp_total_bits"]
+    assert close(float(dbg["err"].sum()), g["zfp_err_sum"], rel=1e-9)
+    assert g["value_range"] == float(x.max()) - float(x.min())
+    # oracle's entropy of the GPU histogram (K3 at full size)
+    assert close(orc.entropy(dbg["hist"]), g["sz_entropy"])
+    _sampled_block_check(orc, x, g, dbg, st)
+    if full_oracle:
+        o = orc.estimate(x, eb, mode="rel", stride=stride)
+        compare_scalars(g, o, tag)
+    return g
+
+
+def test_full_config2_fields(sel, orc):
+    import synth
+    for i in (0, 7):
+        x = synth.c2_field(i)
+        _full_size_check(sel, orc, x, 1e-4, tag=f"C2full{i}")
+        _full_size_check(sel, orc, x, 1e-4, stride=(1, 10), tag=f"C2s{i}")
+
+
+def test_full_config3_field(sel, orc):
+    import synth
+    x = synth.c3_field(5)                 # zero-heavy
+    for eb in (1e-3, 1e-5):
+        _full_size_check(sel, orc, x, eb, tag=f"C3full/{eb}")
+
+
+def test_full_config4_field(sel, orc):
+    import synth
+    x = synth.c4_field(0)                 # heavy-tailed lognormal, VR ~ 1e6
+    _full_size_check(sel, orc, x, 1e-4, stride=(4, 4, 4), tag="C4s")
+    _full_size_check(sel, orc, x, 1e-4, full_oracle=True, tag="C4full")
+
+
+@pytest.mark.parametrize("mix,eb", [(2, 1e-6), (1, 1e-3)])
+def test_full_config5_field(sel, orc, mix, eb):
+    import synth
+    x = synth.c5_field(mix)
+    g = _full_size_check(sel, orc, x, eb, full_oracle=False, tag=f"C5full{mix}")
+    if mix == 2:
+        assert g["sz_overflow_frac"] > 0.5
