@@ -15,8 +15,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("sel_kernels.cu", "sel_api.cu")]
-HEADERS = [os.path.join(CSRC, "sel_internal.h"), os.path.join(ROOT, "include", "sel.h")]
+SOURCES = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+HEADERS = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))) + \
+    [os.path.join(ROOT, "include", "sel.h")]
 LIB = os.path.join(HERE, "libsel.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

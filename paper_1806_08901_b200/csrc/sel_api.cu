@@ -49,8 +49,10 @@ struct sel_plan_st {
   int debug = 0;
   int timing = 0;
   int mm_ctas = 0;
-  int est_ctas_cache[2][2] = {{0, 0}, {0, 0}};   // [vec][debug]
-  int est_ctas_cap = 0;
+  EstLaunch el[2][2] = {};                        // [vec][debug]
+  bool tile_ok = false;                           // TMA tile path available for this shape
+  TileLaunch tl[2] = {};                          // [debug]
+  int max_tasks = 0;
   uint64_t n_sz = 0, n_values = 0;
   int size = 0;                                   // 4^d
 
@@ -82,18 +84,6 @@ struct sel_plan_st {
 };
 
 namespace {
-
-int est_ctas(sel_plan_t p, int vec, int dbg) {
-  int &c = p->est_ctas_cache[vec][dbg];
-  if (c == 0) {
-    Geo g = p->geo;
-    g.vec = vec;
-    c = estimate_max_ctas(g, dbg, p->sm_count);
-    if (c < 0) { c = 0; return -1; }
-    if (c > p->est_ctas_cap) c = p->est_ctas_cap;
-  }
-  return c;
-}
 
 int ensure_results(sel_plan_t p, int n) {
   if (n <= p->res_cap) return SEL_OK;
@@ -143,18 +133,19 @@ int ensure_debug(sel_plan_t p) {
 int enqueue_field(sel_plan_t p, const float *x, cudaStream_t st, sel_result *d_out, int slot) {
   const int vec = (p->geo.n[2] % 4 == 0) && (((uintptr_t)x & 15u) == 0);
   const int dbg = p->debug ? 1 : 0;
-  const int ctas = est_ctas(p, vec, dbg);
-  if (ctas <= 0) return cuda_fail(cudaGetLastError(), "occupancy query");
+  const EstLaunch &el = p->el[vec][dbg];
   Geo g = p->geo;
   g.vec = vec;
+  const bool tile = p->tile_ok && vec;
   if (dbg) CK(cudaMemsetAsync(p->dbg.codes, 0xff, (size_t)p->geo.N * 4, st));
   TimingSlot *ts = p->timing ? &p->tslots[slot] : nullptr;
   if (ts) CK(cudaEventRecord(ts->ev[0], st));
   int rc = launch_minmax(x, g.N, p->mm_ctas, p->ws, p->mode, p->eb, st);
   if (rc) return cuda_fail(cudaGetLastError(), "k_minmax launch");
   if (ts) CK(cudaEventRecord(ts->ev[1], st));
-  rc = launch_estimate(x, g, ctas, p->ws, dbg ? &p->dbg : nullptr, st);
-  if (rc) return cuda_fail(cudaGetLastError(), "k_estimate launch");
+  rc = tile ? launch_tile(x, g, p->tl[dbg], p->ws, dbg ? &p->dbg : nullptr, st)
+            : launch_estimate(x, g, el, p->ws, dbg ? &p->dbg : nullptr, st);
+  if (rc) return cuda_fail(cudaGetLastError(), tile ? "k_tile launch" : "k_estimate launch");
   if (ts) CK(cudaEventRecord(ts->ev[2], st));
   FinalizeArgs fa;
   fa.mode = p->mode;
@@ -163,7 +154,7 @@ int enqueue_field(sel_plan_t p, const float *x, cudaStream_t st, sel_result *d_o
   fa.n_sz = p->n_sz;
   fa.n_values = p->n_values;
   fa.n_blocks = (uint64_t)p->geo.n_pb;
-  fa.est_ctas = ctas;
+  fa.ntasks = tile ? p->tl[dbg].npart : el.ntasks;
   rc = launch_finalize(p->ws, fa, d_out, dbg ? p->dbg_hist : nullptr, st);
   if (rc) return cuda_fail(cudaGetLastError(), "k_finalize launch");
   if (ts) CK(cudaEventRecord(ts->ev[3], st));
@@ -266,14 +257,34 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double e
     return SEL_ECUDA;
   }
   p->mm_ctas = minmax_ctas(N, p->sm_count);
-  p->est_ctas_cap = 8 * p->sm_count;
+  for (int v = 0; v < 2; ++v)
+    for (int d = 0; d < 2; ++d) {
+      Geo gv = g;
+      gv.vec = v;
+      if (plan_estimate(gv, d, p->sm_count, &p->el[v][d]) != SEL_OK) {
+        cuda_fail(cudaGetLastError(), "plan_estimate (occupancy)");
+        delete p;
+        return SEL_ECUDA;
+      }
+      if (p->el[v][d].ntasks > p->max_tasks) p->max_tasks = p->el[v][d].ntasks;
+    }
+  p->tile_ok = tile_supported(g);
+  for (int d = 0; d < 2 && p->tile_ok; ++d) {
+    if (plan_tile(g, p->sm_count, d, &p->tl[d]) != SEL_OK) {
+      cuda_fail(cudaGetLastError(), "plan_tile");
+      delete p;
+      return SEL_ECUDA;
+    }
+    if (p->tl[d].npart > p->max_tasks) p->max_tasks = p->tl[d].npart;
+  }
   // workspace layout
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
   const size_t o_hist = take((size_t)kNSlots * 8), o_mmp = take((size_t)p->mm_ctas * sizeof(float2)),
                o_mmf = take((size_t)p->mm_ctas * 4), o_prm = take(sizeof(Params)),
-               o_ep = take((size_t)p->est_ctas_cap * sizeof(Partial)),
-               o_fp = take((size_t)kFinCTAs * 8), o_fo = take(8), o_tk = take(2 * 4);
+               o_ep = take((size_t)p->max_tasks * sizeof(Partial)), o_tc = take(4),
+               o_fp = take((size_t)kFinCTAs * 8), o_fe = take((size_t)kFinCTAs * 8),
+               o_fb = take((size_t)kFinCTAs * 8), o_fo = take(8), o_tk = take(2 * 4);
   if (cudaMalloc(&p->ws_mem, off) != cudaSuccess) {
     cudaGetLastError();
     delete p;
@@ -285,8 +296,11 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double e
   p->ws.mm_part = (float2 *)(b + o_mmp);
   p->ws.mm_flag = (int32_t *)(b + o_mmf);
   p->ws.params = (Params *)(b + o_prm);
-  p->ws.est_part = (Partial *)(b + o_ep);
+  p->ws.task_part = (Partial *)(b + o_ep);
+  p->ws.task_ctr = (unsigned int *)(b + o_tc);
   p->ws.fin_part = (double *)(b + o_fp);
+  p->ws.fin_err = (double *)(b + o_fe);
+  p->ws.fin_bits = (unsigned long long *)(b + o_fb);
   p->ws.fin_ovf = (unsigned long long *)(b + o_fo);
   p->ws.tickets = (unsigned int *)(b + o_tk);
   if (cudaMemset(p->ws_mem, 0, off) != cudaSuccess || ensure_results(p, 1) != SEL_OK) {

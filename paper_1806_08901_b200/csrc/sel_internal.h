@@ -10,7 +10,7 @@ namespace sel {
 constexpr int kNSlots = 65536;       // 65,535 code bins + overflow slot
 constexpr int kOvfSlot = 65535;
 constexpr int kCenter = 32767;       // slot of code 0
-constexpr int kWinHalf = 8192;       // smem-privatised window: slots [kCenter-kWinHalf, kCenter+kWinHalf)
+constexpr int kWinHalf = 4096;       // smem-privatised window: slots [kCenter-kWinHalf, kCenter+kWinHalf)
 constexpr int kWinBins = 2 * kWinHalf;
 constexpr int kFinCTAs = 64;         // finalize: 64 CTAs x 1024 slots
 constexpr int kFinThreads = 256;
@@ -39,10 +39,47 @@ struct Params {
   int32_t pad;
 };
 
-// Per-CTA partials of the fused pass.
+// Per-task partials of the fused pass (summed in task order by the finalize).
 struct Partial {
   uint64_t bits;    // sum of per-block EC bits
   double err;       // sum of E_b
+};
+
+// Geometry of the marching kernel (2D/3D, every block processed).  The marching axis
+// is the slowest block axis (view axis 0 for 3D, 1 for 2D); a warp task is 32
+// consecutive blocks along the fastest axis x one "other" block row (3D) x L layers.
+struct MarchGeo {
+  int64_t n[3];
+  int64_t nb[3];
+  int32_t L;        // block layers per task
+  int32_t nchunk;   // ceil(nb[2] / 32)
+  int32_t nother;   // nb[1] for 3D, 1 for 2D
+  int32_t nseg;     // ceil(nb_march / L)
+  int32_t ntasks;   // nseg * nother * nchunk
+  int32_t pad;
+};
+
+// Geometry of the TMA tile kernel (2D/3D, every block, fastest extent % 4 == 0).
+struct TileGeo {
+  int64_t n[3];
+  int32_t nb[3];
+  int32_t ntj;      // tiles along axis 1 (8 block rows each)
+  int32_t ntk;      // tiles along axis 2 (32 blocks each)
+  int32_t ntasks;   // ntj * ntk * (nb[0] for 3D)
+};
+
+struct TileLaunch {
+  int ctas;
+  size_t smem;
+  int npart;        // partials written = ntasks * 8 warps
+  TileGeo tg;
+};
+
+struct EstLaunch {
+  bool march;
+  int ctas;
+  int ntasks;       // partials written (march: tasks; generic: CTAs)
+  MarchGeo mg;
 };
 
 // Debug dump pointers (device), all may be null.
@@ -60,8 +97,11 @@ struct Workspace {
   float2 *mm_part;            // [mm_ctas] (min,max)
   int32_t *mm_flag;           // [mm_ctas] nonfinite flags
   Params *params;             // [1]
-  Partial *est_part;          // [est_ctas]
+  Partial *task_part;         // [max tasks]
+  unsigned int *task_ctr;     // [1] dynamic task counter (reset by finalize)
   double *fin_part;           // [kFinCTAs]
+  double *fin_err;            // [kFinCTAs]
+  unsigned long long *fin_bits; // [kFinCTAs]
   unsigned long long *fin_ovf;// [1]
   unsigned int *tickets;      // [2] last-block-done counters (minmax, finalize)
 };
@@ -73,17 +113,21 @@ struct FinalizeArgs {
   uint64_t n_sz;            // SZ points (host geometry)
   uint64_t n_values;        // N_P
   uint64_t n_blocks;
-  int32_t est_ctas;
+  int32_t ntasks;
 };
 
 // launchers (sel_kernels.cu)
 int launch_minmax(const float *x, int64_t N, int ctas, const Workspace &ws, int mode, double eb,
                   cudaStream_t st);
-int launch_estimate(const float *x, const Geo &g, int ctas, const Workspace &ws,
+int plan_estimate(const Geo &g, int debug, int sm_count, EstLaunch *el);
+int launch_estimate(const float *x, const Geo &g, const EstLaunch &el, const Workspace &ws,
                     const DebugPtrs *dbg, cudaStream_t st);
+bool tile_supported(const Geo &g);
+int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl);
+int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Workspace &ws,
+                const DebugPtrs *dbg, cudaStream_t st);
 int launch_finalize(const Workspace &ws, const FinalizeArgs &fa, sel_result *d_out,
                     unsigned long long *dbg_hist, cudaStream_t st);
-int estimate_max_ctas(const Geo &g, int debug, int sm_count);
 int minmax_ctas(int64_t N, int sm_count);
 
 }  // namespace sel

@@ -68,13 +68,13 @@ def check_case(sel, orc, x, eb, mode="rel", stride=None, offset_elems=0, tag="")
     for k in ("codes", "hist", "emax", "coef", "uword", "bits"):
         assert np.array_equal(gd[k].reshape(od[k].shape), od[k]), (tag, k)
     assert np.allclose(gd["err"], od["err"], rtol=1e-12, atol=0), tag
-    # the non-debug instantiation (the one bench.py times) gives the same result
+    # the non-debug instantiation (the one bench.py times) agrees with the oracle
+    # and is deterministic run to run (fixed tile -> partial mapping)
     g2, _ = run_gpu(sel, x, eb, mode, stride, debug=False, offset_elems=offset_elems)
+    g3, _ = run_gpu(sel, x, eb, mode, stride, debug=False, offset_elems=offset_elems)
     compare_scalars(g2, o, tag + "/nodebug")
-    for k in g:
-        if isinstance(g[k], float) and math.isnan(g[k]):
-            continue
-        assert g2[k] == g[k], (tag, k)          # deterministic run to run
+    for k in g2:
+        assert g2[k] == g3[k] or (isinstance(g2[k], float) and math.isnan(g2[k])), (tag, k)
     # host-side Alg. 1 recomputation agrees with the device's choice
     assert sel.choose(g) == g["choice"]
     return g, o
@@ -277,8 +277,11 @@ def _full_size_check(sel, orc, x, eb, stride=None, full_oracle=True, tag=""):
         p.set_option("debug", 1)
         gd = p.estimate(t)
         dbg = {k: p.debug_copy(k) for k in ("codes", "hist", "emax", "coef", "uword", "bits", "err")}
-    for k in g:
-        assert g[k] == gd[k] or (isinstance(g[k], float) and math.isnan(g[k])), (tag, k)
+    for k in g:      # debug build may use another grid: double sums agree to rounding
+        if isinstance(g[k], float):
+            assert close(g[k], gd[k], rel=1e-12), (tag, k)
+        else:
+            assert g[k] == gd[k], (tag, k)
     # properties at any size
     assert int(dbg["hist"].sum()) == g["n_sz_points"]
     assert int(dbg["bits"].astype(np.uint64).sum()) == g["zfp_total_bits"]
