@@ -58,7 +58,8 @@ struct sel_plan_st {
 
   void *ws_mem = nullptr;
   size_t ws_bytes = 0;
-  Workspace ws{};
+  Workspace ws{};          // parity-0 copy (sequential path)
+  Workspace wsk[2]{};      // per field parity (batch pipeline)
 
   sel_result *d_res = nullptr;
   sel_result *h_res = nullptr;   // pinned
@@ -75,6 +76,12 @@ struct sel_plan_st {
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
 
+  // per-field params (capacity res_cap) and the batch pipeline's aux stream/events
+  Params *d_params = nullptr;
+  cudaStream_t aux_stream = nullptr, fin_stream = nullptr;
+  std::vector<cudaEvent_t> ev_mm, ev_k2, ev_k3;
+  int pipeline = 1;
+
   // kernel timing
   std::vector<TimingSlot> tslots;
   double ms[3] = {0, 0, 0};
@@ -89,11 +96,14 @@ int ensure_results(sel_plan_t p, int n) {
   if (n <= p->res_cap) return SEL_OK;
   if (p->d_res) cudaFree(p->d_res);
   if (p->h_res) cudaFreeHost(p->h_res);
+  if (p->d_params) cudaFree(p->d_params);
   p->d_res = nullptr;
   p->h_res = nullptr;
+  p->d_params = nullptr;
   p->res_cap = 0;
   CK(cudaMalloc(&p->d_res, sizeof(sel_result) * (size_t)n));
   CK(cudaMallocHost(&p->h_res, sizeof(sel_result) * (size_t)n));
+  CK(cudaMalloc(&p->d_params, sizeof(Params) * (size_t)n));
   p->res_cap = n;
   return SEL_OK;
 }
@@ -129,22 +139,34 @@ int ensure_debug(sel_plan_t p) {
   return SEL_OK;
 }
 
-// Enqueue K1 -> K2 -> K3 for one field; result lands in d_out.
-int enqueue_field(sel_plan_t p, const float *x, cudaStream_t st, sel_result *d_out, int slot) {
+// Per-field launches.  Each field f owns params slot f (written by its k_minmax, read
+// by its fused pass and finalize), so value-range passes may run ahead of the fused
+// passes of earlier fields on another stream (batch pipeline below).
+Workspace field_ws(sel_plan_t p, int f, int parity = 0) {
+  Workspace w = p->wsk[parity];
+  w.params = p->d_params + f;
+  return w;
+}
+
+int enqueue_minmax(sel_plan_t p, const float *x, int f, cudaStream_t st) {
+  const Workspace w = field_ws(p, f);
+  int rc = launch_minmax(x, p->geo.N, p->mm_ctas, w, p->mode, p->eb, st);
+  if (rc) return cuda_fail(cudaGetLastError(), "k_minmax launch");
+  p->launches += 1;
+  return SEL_OK;
+}
+
+int enqueue_est(sel_plan_t p, const float *x, int f, cudaStream_t st, TimingSlot *ts,
+                int parity = 0, cudaStream_t fin_st = nullptr, cudaEvent_t k2_done = nullptr) {
   const int vec = (p->geo.n[2] % 4 == 0) && (((uintptr_t)x & 15u) == 0);
   const int dbg = p->debug ? 1 : 0;
   const EstLaunch &el = p->el[vec][dbg];
   Geo g = p->geo;
   g.vec = vec;
   const bool tile = p->tile_ok && vec;
-  if (dbg) CK(cudaMemsetAsync(p->dbg.codes, 0xff, (size_t)p->geo.N * 4, st));
-  TimingSlot *ts = p->timing ? &p->tslots[slot] : nullptr;
-  if (ts) CK(cudaEventRecord(ts->ev[0], st));
-  int rc = launch_minmax(x, g.N, p->mm_ctas, p->ws, p->mode, p->eb, st);
-  if (rc) return cuda_fail(cudaGetLastError(), "k_minmax launch");
-  if (ts) CK(cudaEventRecord(ts->ev[1], st));
-  rc = tile ? launch_tile(x, g, p->tl[dbg], p->ws, dbg ? &p->dbg : nullptr, st)
-            : launch_estimate(x, g, el, p->ws, dbg ? &p->dbg : nullptr, st);
+  const Workspace w = field_ws(p, f, parity);
+  int rc = tile ? launch_tile(x, g, p->tl[dbg], w, dbg ? &p->dbg : nullptr, st)
+                : launch_estimate(x, g, el, w, dbg ? &p->dbg : nullptr, st);
   if (rc) return cuda_fail(cudaGetLastError(), tile ? "k_tile launch" : "k_estimate launch");
   if (ts) CK(cudaEventRecord(ts->ev[2], st));
   FinalizeArgs fa;
@@ -155,10 +177,76 @@ int enqueue_field(sel_plan_t p, const float *x, cudaStream_t st, sel_result *d_o
   fa.n_values = p->n_values;
   fa.n_blocks = (uint64_t)p->geo.n_pb;
   fa.ntasks = tile ? p->tl[dbg].npart : el.ntasks;
-  rc = launch_finalize(p->ws, fa, d_out, dbg ? p->dbg_hist : nullptr, st);
+  if (k2_done) {                      // finalize on its own stream, after this fused pass
+    CK(cudaEventRecord(k2_done, st));
+    CK(cudaStreamWaitEvent(fin_st, k2_done, 0));
+    st = fin_st;
+  }
+  rc = launch_finalize(w, fa, p->d_res + f, dbg ? p->dbg_hist : nullptr, st);
   if (rc) return cuda_fail(cudaGetLastError(), "k_finalize launch");
   if (ts) CK(cudaEventRecord(ts->ev[3], st));
-  p->launches += 3;
+  p->launches += 2;
+  return SEL_OK;
+}
+
+// Sequential K1 -> K2 -> K3 for one field on one stream; result lands in d_res[f].
+int enqueue_field(sel_plan_t p, const float *x, cudaStream_t st, int f) {
+  if (p->debug) CK(cudaMemsetAsync(p->dbg.codes, 0xff, (size_t)p->geo.N * 4, st));
+  TimingSlot *ts = p->timing ? &p->tslots[f] : nullptr;
+  if (ts) CK(cudaEventRecord(ts->ev[0], st));
+  int rc = enqueue_minmax(p, x, f, st);
+  if (rc) return rc;
+  if (ts) CK(cudaEventRecord(ts->ev[1], st));
+  return enqueue_est(p, x, f, st, ts);
+}
+
+int ensure_aux(sel_plan_t p, int n) {
+  if (!p->aux_stream) CK(cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking));
+  if (!p->fin_stream) CK(cudaStreamCreateWithFlags(&p->fin_stream, cudaStreamNonBlocking));
+  while ((int)p->ev_mm.size() < n + 1) {
+    cudaEvent_t a, b, c;
+    CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+    p->ev_mm.push_back(a);
+    p->ev_k2.push_back(b);
+    p->ev_k3.push_back(c);
+  }
+  return SEL_OK;
+}
+
+// Batch pipeline over three streams.  aux: k_minmax(f) (DRAM-bound, one small CTA per
+// SM); main: the fused pass of f (ALU-bound, one persistent CTA per SM); fin: finalize
+// of f (latency-bound).  The three kinds co-reside on the SMs, so the value range of
+// f+1 and the finalize of f-1 run under the fused pass of f; field f+1 is left in L2
+// for its own fused pass.  k_minmax(f+2) is released by the fused pass of f (at most one
+// field runs ahead); the fused pass of f+2 waits for the finalize of f, the other user
+// of its parity's workspace.
+int enqueue_pipelined(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
+  int rc = ensure_aux(p, n);
+  if (rc) return rc;
+  cudaEvent_t start = p->ev_mm[n];
+  CK(cudaEventRecord(start, st));                 // prior work on the caller's stream
+  CK(cudaStreamWaitEvent(p->aux_stream, start, 0));
+  CK(cudaStreamWaitEvent(p->fin_stream, start, 0));
+  auto minmax = [&](int f) -> int {
+    if (f >= 2) CK(cudaStreamWaitEvent(p->aux_stream, p->ev_k2[f - 2], 0));
+    int r = enqueue_minmax(p, x[f], f, p->aux_stream);
+    if (r) return r;
+    CK(cudaEventRecord(p->ev_mm[f], p->aux_stream));
+    return SEL_OK;
+  };
+  if ((rc = minmax(0))) return rc;
+  if (n > 1 && (rc = minmax(1))) return rc;
+  for (int f = 0; f < n; ++f) {
+    CK(cudaStreamWaitEvent(st, p->ev_mm[f], 0));
+    if (f >= 2) CK(cudaStreamWaitEvent(st, p->ev_k3[f - 2], 0));
+    if ((rc = enqueue_est(p, x[f], f, st, nullptr, f & 1, p->fin_stream, p->ev_k2[f]))) return rc;
+    CK(cudaEventRecord(p->ev_k3[f], p->fin_stream));
+    if (f + 2 < n && (rc = minmax(f + 2))) return rc;
+  }
+  CK(cudaStreamWaitEvent(st, p->ev_k3[n - 1], 0));   // results complete on the caller's stream
+  CK(cudaStreamWaitEvent(st, p->ev_mm[n - 1], 0));
   return SEL_OK;
 }
 
@@ -277,14 +365,23 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double e
     }
     if (p->tl[d].npart > p->max_tasks) p->max_tasks = p->tl[d].npart;
   }
-  // workspace layout
+  // workspace layout: two copies (field parity) of the fused-pass/finalize state so
+  // the finalize of field f can overlap the fused pass of field f+1 (batch pipeline)
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
-  const size_t o_hist = take((size_t)kNSlots * 8), o_mmp = take((size_t)p->mm_ctas * sizeof(float2)),
-               o_mmf = take((size_t)p->mm_ctas * 4), o_prm = take(sizeof(Params)),
-               o_ep = take((size_t)p->max_tasks * sizeof(Partial)), o_tc = take(4),
-               o_fp = take((size_t)kFinCTAs * 8), o_fe = take((size_t)kFinCTAs * 8),
-               o_fb = take((size_t)kFinCTAs * 8), o_fo = take(8), o_tk = take(2 * 4);
+  size_t o_hist[2], o_ep[2], o_tc[2], o_fp[2], o_fe[2], o_fb[2], o_fo[2], o_tk[2];
+  const size_t o_mmp = take((size_t)p->mm_ctas * sizeof(float2)), o_mmf = take((size_t)p->mm_ctas * 4),
+               o_prm = take(sizeof(Params));
+  for (int k = 0; k < 2; ++k) {
+    o_hist[k] = take((size_t)kNSlots * 8);
+    o_ep[k] = take((size_t)p->max_tasks * sizeof(Partial));
+    o_tc[k] = take(4);
+    o_fp[k] = take((size_t)kFinCTAs * 8);
+    o_fe[k] = take((size_t)kFinCTAs * 8);
+    o_fb[k] = take((size_t)kFinCTAs * 8);
+    o_fo[k] = take(8);
+    o_tk[k] = take(2 * 4);
+  }
   if (cudaMalloc(&p->ws_mem, off) != cudaSuccess) {
     cudaGetLastError();
     delete p;
@@ -292,17 +389,21 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double e
   }
   p->ws_bytes = off;
   char *b = (char *)p->ws_mem;
-  p->ws.hist = (unsigned long long *)(b + o_hist);
-  p->ws.mm_part = (float2 *)(b + o_mmp);
-  p->ws.mm_flag = (int32_t *)(b + o_mmf);
-  p->ws.params = (Params *)(b + o_prm);
-  p->ws.task_part = (Partial *)(b + o_ep);
-  p->ws.task_ctr = (unsigned int *)(b + o_tc);
-  p->ws.fin_part = (double *)(b + o_fp);
-  p->ws.fin_err = (double *)(b + o_fe);
-  p->ws.fin_bits = (unsigned long long *)(b + o_fb);
-  p->ws.fin_ovf = (unsigned long long *)(b + o_fo);
-  p->ws.tickets = (unsigned int *)(b + o_tk);
+  for (int k = 0; k < 2; ++k) {
+    Workspace &w = p->wsk[k];
+    w.hist = (unsigned long long *)(b + o_hist[k]);
+    w.mm_part = (float2 *)(b + o_mmp);
+    w.mm_flag = (int32_t *)(b + o_mmf);
+    w.params = (Params *)(b + o_prm);
+    w.task_part = (Partial *)(b + o_ep[k]);
+    w.task_ctr = (unsigned int *)(b + o_tc[k]);
+    w.fin_part = (double *)(b + o_fp[k]);
+    w.fin_err = (double *)(b + o_fe[k]);
+    w.fin_bits = (unsigned long long *)(b + o_fb[k]);
+    w.fin_ovf = (unsigned long long *)(b + o_fo[k]);
+    w.tickets = (unsigned int *)(b + o_tk[k]);
+  }
+  p->ws = p->wsk[0];
   if (cudaMemset(p->ws_mem, 0, off) != cudaSuccess || ensure_results(p, 1) != SEL_OK) {
     cuda_fail(cudaGetLastError(), "workspace init");
     sel_plan_destroy(p);
@@ -324,6 +425,10 @@ int sel_set_option(sel_plan_t p, const char *key, double value) {
     if (p->debug) return ensure_debug(p);
     return SEL_OK;
   }
+  if (!strcmp(key, "pipeline")) {
+    p->pipeline = value != 0.0;
+    return SEL_OK;
+  }
   if (!strcmp(key, "kernel_timing")) {
     p->timing = value != 0.0;
     return SEL_OK;
@@ -337,7 +442,7 @@ int sel_estimate(sel_plan_t p, const float *d_field, void *stream, sel_result *o
   int rc = ensure_results(p, 1);
   if (rc) return rc;
   if (p->timing && (rc = ensure_timing(p, 1))) return rc;
-  if ((rc = enqueue_field(p, d_field, st, p->d_res, 0))) return rc;
+  if ((rc = enqueue_field(p, d_field, st, 0))) return rc;
   sel_result r;
   if ((rc = finish(p, st, 1, &r))) return rc;
   if (r.status != SEL_OK) return r.status;
@@ -354,8 +459,12 @@ int sel_estimate_batch(sel_plan_t p, const float *const *d_fields, int n, void *
   int rc = ensure_results(p, n);
   if (rc) return rc;
   if (p->timing && (rc = ensure_timing(p, n))) return rc;
-  for (int f = 0; f < n; ++f)
-    if ((rc = enqueue_field(p, d_fields[f], st, p->d_res + f, f))) return rc;
+  if (n >= 2 && p->pipeline && !p->timing && !p->debug) {
+    if ((rc = enqueue_pipelined(p, d_fields, n, st))) return rc;
+  } else {
+    for (int f = 0; f < n; ++f)
+      if ((rc = enqueue_field(p, d_fields[f], st, f))) return rc;
+  }
   return finish(p, st, n, out);
 }
 
@@ -385,7 +494,7 @@ int sel_estimate_batch_host(sel_plan_t p, const float *const *h_fields, int n, v
     CK(cudaMemcpyAsync(p->d_stage[b], h_fields[f], bytes, cudaMemcpyHostToDevice, p->copy_stream));
     CK(cudaEventRecord(p->ev_copied[b], p->copy_stream));
     CK(cudaStreamWaitEvent(st, p->ev_copied[b], 0));
-    if ((rc = enqueue_field(p, p->d_stage[b], st, p->d_res + f, f))) return rc;
+    if ((rc = enqueue_field(p, p->d_stage[b], st, f))) return rc;
     CK(cudaEventRecord(p->ev_done[b], st));
   }
   return finish(p, st, n, out);
@@ -449,6 +558,18 @@ void sel_plan_destroy(sel_plan_t p) {
     if (p->ev_done[b]) cudaEventDestroy(p->ev_done[b]);
   }
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->aux_stream) {
+    cudaStreamSynchronize(p->aux_stream);
+    cudaStreamDestroy(p->aux_stream);
+  }
+  if (p->fin_stream) {
+    cudaStreamSynchronize(p->fin_stream);
+    cudaStreamDestroy(p->fin_stream);
+  }
+  for (auto e : p->ev_mm) cudaEventDestroy(e);
+  for (auto e : p->ev_k2) cudaEventDestroy(e);
+  for (auto e : p->ev_k3) cudaEventDestroy(e);
+  if (p->d_params) cudaFree(p->d_params);
   for (auto &s : p->tslots)
     for (auto &e : s.ev) cudaEventDestroy(e);
   delete p;

@@ -13,7 +13,7 @@ constexpr int kCenter = 32767;       // slot of code 0
 constexpr int kWinHalf = 4096;       // smem-privatised window: slots [kCenter-kWinHalf, kCenter+kWinHalf)
 constexpr int kWinBins = 2 * kWinHalf;
 constexpr int kFinCTAs = 64;         // finalize: 64 CTAs x 1024 slots
-constexpr int kFinThreads = 256;
+constexpr int kFinThreads = 128;
 
 // Geometry, padded to 3 axes: axis 0 slowest.  For ndims < 3 the leading axes
 // have n = nb = npb = s = 1.
@@ -63,15 +63,16 @@ struct MarchGeo {
 struct TileGeo {
   int64_t n[3];
   int32_t nb[3];
-  int32_t ntj;      // tiles along axis 1 (8 block rows each)
+  int32_t ntj;      // tiles along axis 1 (one block row per consumer warp)
   int32_t ntk;      // tiles along axis 2 (32 blocks each)
   int32_t ntasks;   // ntj * ntk * (nb[0] for 3D)
 };
 
 struct TileLaunch {
   int ctas;
+  int threads;
   size_t smem;
-  int npart;        // partials written = ntasks * 8 warps
+  int npart;        // partials written = ntasks * consumer warps
   TileGeo tg;
 };
 

@@ -130,8 +130,7 @@ __global__ void __launch_bounds__(THREADS) k_minmax(const float *__restrict__ x,
     int e = 0;
     frexp(p.eb_abs, &e);
     p.minexp = e - 1;                                     // floor(log2 eb_abs)
-    grid_dep_wait();   // the previous field's finalize may still read params
-    *ws.params = p;
+    *ws.params = p;    // this field's own params slot
     ws.tickets[0] = 0;
   }
 }
@@ -489,9 +488,15 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
   const double Nsz = (double)fa.n_sz;
   const double lN = log2(Nsz);
   double acc = 0.0;
-  constexpr int PER = kNSlots / kFinCTAs;
-  for (int s = blockIdx.x * PER + threadIdx.x; s < (blockIdx.x + 1) * PER; s += kFinThreads) {
-    const unsigned long long c = ws.hist[s];
+  constexpr int PER = kNSlots / kFinCTAs;            // 1024 slots per CTA
+  constexpr int SPT = PER / kFinThreads;             // slots per thread, all loads in flight
+  unsigned long long cs[SPT];
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) cs[k] = __ldcg(ws.hist + blockIdx.x * PER + k * kFinThreads + threadIdx.x);
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    const int s = blockIdx.x * PER + k * kFinThreads + threadIdx.x;
+    const unsigned long long c = cs[k];
     if (c) {
       const double cd = (double)c;
       acc += cd * (lN - log2(cd));          // c log2(N/c): exactly 0 for a single slot
@@ -506,6 +511,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
   {
     const int per = (fa.ntasks + kFinCTAs - 1) / kFinCTAs;
     const int t0 = blockIdx.x * per, t1 = min(t0 + per, fa.ntasks);
+#pragma unroll 4
     for (int t = t0 + threadIdx.x; t < t1; t += kFinThreads) {
       bits += __ldcg(&ws.task_part[t].bits);
       err += __ldcg(&ws.task_part[t].err);
@@ -533,8 +539,33 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
     last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
+  // ---- last CTA: fixed-order reduction of the 64 CTA partials (warps 0-1), and the
+  // independent transcendentals spread over threads, then thread 0 assembles the result
   __threadfence();
+  __shared__ double sfin[4];
+  __shared__ uint64_t sfb[2];
+  __shared__ double slog[3];
+  if (threadIdx.x < kFinCTAs) {
+    double a = __ldcg(ws.fin_part + threadIdx.x), e = __ldcg(ws.fin_err + threadIdx.x);
+    uint64_t tb = __ldcg(ws.fin_bits + threadIdx.x);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      e += __shfl_down_sync(0xffffffffu, e, o);
+      tb += __shfl_down_sync(0xffffffffu, tb, o);
+    }
+    if (lane == 0) { sfin[wid * 2] = a; sfin[wid * 2 + 1] = e; sfb[wid] = tb; }
+  }
+  __syncthreads();
+  const double vr = prm.vr, eb = prm.eb_abs;
+  const double errs = sfin[1] + sfin[3];
+  const double mse = errs / (double)fa.n_values;
+  if (threadIdx.x == 32) slog[0] = log10(vr / eb);
+  if (threadIdx.x == 64) slog[1] = log10(vr);
+  if (threadIdx.x == 96) slog[2] = mse > 0.0 ? log10(mse) : 0.0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   ws.tickets[1] = 0;
   *ws.task_ctr = 0;
 
@@ -549,26 +580,20 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
   r.n_blocks = fa.n_blocks;
   if (r.status == SEL_OK && fa.n_sz == 0) r.status = SEL_EDEGENERATE;   // single-value field
   if (r.status == SEL_OK) {
-    double S = 0.0, errs = 0.0;
-    uint64_t tb = 0;
-    for (int b = 0; b < kFinCTAs; ++b) {
-      S += __ldcg(ws.fin_part + b);
-      errs += __ldcg(ws.fin_err + b);
-      tb += __ldcg(ws.fin_bits + b);
-    }
-    const double vr = prm.vr, eb = prm.eb_abs;
+    const double S = sfin[0] + sfin[2];
+    const uint64_t tb = sfb[0] + sfb[1];
     const double H = S / Nsz;                                        // Eq. entropy
     const double povf = (double)__ldcg(ws.fin_ovf) / Nsz;
     r.sz_entropy = H;
     r.sz_overflow_frac = povf;
     r.sz_bits_per_value = H + fa.sz_offset + 32.0 * povf;            // P:402, R6
-    r.sz_psnr = 20.0 * log10(vr / eb) + 10.0 * log10(3.0);           // Eq. psnr-sz
+    r.sz_psnr = 20.0 * slog[0] + 10.0 * log10(3.0);                  // Eq. psnr-sz
     r.zfp_total_bits = tb;
     r.zfp_err_sum = errs;
     r.zfp_bits_per_value = (double)tb / (double)fa.n_values;
-    r.zfp_mse = errs / (double)fa.n_values;
-    r.zfp_psnr = r.zfp_mse > 0.0 ? 20.0 * log10(vr) - 10.0 * log10(r.zfp_mse)
-                                 : __longlong_as_double(0x7ff0000000000000LL);
+    r.zfp_mse = mse;
+    r.zfp_psnr = mse > 0.0 ? 20.0 * slog[1] - 10.0 * slog[2]
+                           : __longlong_as_double(0x7ff0000000000000LL);
     // Alg.1 lines 7-10 (R16)
     if (!(r.zfp_mse > 0.0) || !(vr > 0.0) || !isfinite(r.zfp_psnr)) {
       r.matched = 0;
@@ -604,18 +629,18 @@ static cudaError_t launch_pdl(const void *fn, dim3 grid, dim3 block, size_t smem
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
+// One 256-thread CTA per SM at most: small enough (regs, no smem) to co-reside with the
+// persistent fused-pass CTA, so the batch pipeline can overlap the two.
 int minmax_ctas(int64_t N, int sm_count) {
-  int64_t want = (N + 512 * 32 - 1) / (512 * 32);
-  int64_t cap = 2LL * sm_count;
+  int64_t want = (N + 256 * 32 - 1) / (256 * 32);
+  int64_t cap = sm_count;
   return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
 int launch_minmax(const float *x, int64_t N, int ctas, const Workspace &ws, int mode, double eb,
                   cudaStream_t st) {
-  Workspace w = ws;
-  void *args[] = {(void *)&x, (void *)&N, (void *)&w, (void *)&mode, (void *)&eb};
-  return launch_pdl((const void *)k_minmax<512>, dim3(ctas), dim3(512), 0, st, args) == cudaSuccess
-             ? SEL_OK : SEL_ECUDA;
+  k_minmax<256><<<ctas, 256, 0, st>>>(x, N, ws, mode, eb);
+  return cudaGetLastError() == cudaSuccess ? SEL_OK : SEL_ECUDA;
 }
 
 template <int D, bool VEC, bool DBG>
