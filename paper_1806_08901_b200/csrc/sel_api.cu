@@ -52,6 +52,12 @@ struct sel_plan_st {
   EstLaunch el[2][2] = {};                        // [vec][debug]
   bool tile_ok = false;                           // TMA tile path available for this shape
   TileLaunch tl[2] = {};                          // [debug]
+  BatchSizes bs{};                                // persistent batch kernel sizes
+  int use_batch = 1;
+  void *bstate = nullptr;                         // batch kernel state (grows with n)
+  cudaEvent_t bev[2] = {nullptr, nullptr};        // kernel_timing around k_batch
+  bool batch_timed = false;
+  size_t bstate_cap = 0;
   int max_tasks = 0;
   uint64_t n_sz = 0, n_values = 0;
   int size = 0;                                   // 4^d
@@ -189,6 +195,51 @@ int enqueue_est(sel_plan_t p, const float *x, int f, cudaStream_t st, TimingSlot
   return SEL_OK;
 }
 
+// One persistent launch for the whole batch (sel_batch.cu): value range, tiles and
+// finalize of every field as one task stream; results land in d_res[0..n).
+bool batch_ok(sel_plan_t p, const float *const *x, int n) {
+  if (!p->tile_ok || !p->use_batch || p->debug) return false;
+  for (int f = 0; f < n; ++f)
+    if (((uintptr_t)x[f] & 15u) != 0) return false;
+  return true;
+}
+
+int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
+  const size_t need = batch_state_bytes(n, p->bs, p->tl[0].tg.ntasks);
+  if (need > p->bstate_cap) {
+    if (p->bstate) {
+      CK(cudaStreamSynchronize(st));
+      cudaFree(p->bstate);
+    }
+    p->bstate = nullptr;
+    p->bstate_cap = 0;
+    if (cudaMalloc(&p->bstate, need) != cudaSuccess) return SEL_ENOMEM;
+    p->bstate_cap = need;
+  }
+  FinalizeArgs fa;
+  fa.mode = p->mode;
+  fa.eb = p->eb;
+  fa.sz_offset = p->sz_offset;
+  fa.n_sz = p->n_sz;
+  fa.n_values = p->n_values;
+  fa.n_blocks = (uint64_t)p->geo.n_pb;
+  fa.ntasks = 0;
+  Geo g = p->geo;
+  g.vec = 1;
+  if (p->timing) {
+    if (!p->bev[0]) {
+      CK(cudaEventCreate(&p->bev[0]));
+      CK(cudaEventCreate(&p->bev[1]));
+    }
+  }
+  int rc = launch_batch(g, p->tl[0], p->bs, x, n, p->bstate, p->bstate_cap, fa, p->mode, p->eb,
+                        p->d_res, p->sm_count, st, p->timing ? p->bev : nullptr);
+  if (rc) return cuda_fail(cudaGetLastError(), "k_batch launch");
+  p->launches += 1;
+  p->batch_timed = p->timing;
+  return SEL_OK;
+}
+
 // Sequential K1 -> K2 -> K3 for one field on one stream; result lands in d_res[f].
 int enqueue_field(sel_plan_t p, const float *x, cudaStream_t st, int f) {
   if (p->debug) CK(cudaMemsetAsync(p->dbg.codes, 0xff, (size_t)p->geo.N * 4, st));
@@ -252,6 +303,14 @@ int enqueue_pipelined(sel_plan_t p, const float *const *x, int n, cudaStream_t s
 
 int collect_timing(sel_plan_t p, int n) {
   if (!p->timing) return SEL_OK;
+  if (p->batch_timed) {           // one k_batch launch: all of it counts as the fused pass
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p->bev[0], p->bev[1]));
+    p->ms[1] += ms;
+    p->tcount[1] += 1;
+    p->batch_timed = false;
+    return SEL_OK;
+  }
   for (int f = 0; f < n; ++f) {
     for (int k = 0; k < 3; ++k) {
       float ms = 0.f;
@@ -365,6 +424,11 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double e
     }
     if (p->tl[d].npart > p->max_tasks) p->max_tasks = p->tl[d].npart;
   }
+  if (p->tile_ok && batch_sizes(g, &p->bs) != SEL_OK) {
+    cuda_fail(cudaGetLastError(), "batch_sizes");
+    delete p;
+    return SEL_ECUDA;
+  }
   // workspace layout: two copies (field parity) of the fused-pass/finalize state so
   // the finalize of field f can overlap the fused pass of field f+1 (batch pipeline)
   size_t off = 0;
@@ -425,6 +489,10 @@ int sel_set_option(sel_plan_t p, const char *key, double value) {
     if (p->debug) return ensure_debug(p);
     return SEL_OK;
   }
+  if (!strcmp(key, "batch_kernel")) {
+    p->use_batch = value != 0.0;
+    return SEL_OK;
+  }
   if (!strcmp(key, "pipeline")) {
     p->pipeline = value != 0.0;
     return SEL_OK;
@@ -442,7 +510,11 @@ int sel_estimate(sel_plan_t p, const float *d_field, void *stream, sel_result *o
   int rc = ensure_results(p, 1);
   if (rc) return rc;
   if (p->timing && (rc = ensure_timing(p, 1))) return rc;
-  if ((rc = enqueue_field(p, d_field, st, 0))) return rc;
+  if (batch_ok(p, &d_field, 1)) {
+    if ((rc = enqueue_batch(p, &d_field, 1, st))) return rc;
+  } else if ((rc = enqueue_field(p, d_field, st, 0))) {
+    return rc;
+  }
   sel_result r;
   if ((rc = finish(p, st, 1, &r))) return rc;
   if (r.status != SEL_OK) return r.status;
@@ -459,7 +531,9 @@ int sel_estimate_batch(sel_plan_t p, const float *const *d_fields, int n, void *
   int rc = ensure_results(p, n);
   if (rc) return rc;
   if (p->timing && (rc = ensure_timing(p, n))) return rc;
-  if (n >= 2 && p->pipeline && !p->timing && !p->debug) {
+  if (batch_ok(p, d_fields, n)) {
+    if ((rc = enqueue_batch(p, d_fields, n, st))) return rc;
+  } else if (n >= 2 && p->pipeline && !p->timing && !p->debug) {
     if ((rc = enqueue_pipelined(p, d_fields, n, st))) return rc;
   } else {
     for (int f = 0; f < n; ++f)
@@ -570,6 +644,9 @@ void sel_plan_destroy(sel_plan_t p) {
   for (auto e : p->ev_k2) cudaEventDestroy(e);
   for (auto e : p->ev_k3) cudaEventDestroy(e);
   if (p->d_params) cudaFree(p->d_params);
+  if (p->bstate) cudaFree(p->bstate);
+  for (auto e : p->bev)
+    if (e) cudaEventDestroy(e);
   for (auto &s : p->tslots)
     for (auto &e : s.ev) cudaEventDestroy(e);
   delete p;

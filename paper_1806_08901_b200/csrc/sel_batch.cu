@@ -1,0 +1,507 @@
+// sel_batch.cu -- one persistent launch for a whole batch of fields (2D/3D tile shapes).
+//
+// The estimate of a field is three dependent phases: value range (needs every value,
+// Alg.1 line 2), the fused SZ+ZFP tile pass (needs eb, r_f, minexp), and the histogram
+// entropy / selection (needs every tile).  Instead of three launches per field, one
+// persistent CTA per SM pulls tasks of three kinds from a single global sequence laid out
+// in phases:   phase p = [ F(p-4) | R(p) and T(p-2) interleaved ]
+//   R(f, i): TMA bulk copy of chunk i of field f into a stage, min/max/non-finite;
+//            the last R task of f writes params(f) and raises params_ready[f]
+//   T(f, i): the TMA tile task of k_tile (same consumer code, sel_tile_common.cuh)
+//   F(f, k): 1/8 of the histogram entropy + tile partials of f (needs tdone[f] == nT);
+//            the last F task of f writes result f and raises fin_ready[f]
+// A task only ever waits (spin on a flag) for tasks earlier in the sequence, every CTA
+// processes its tasks in fetch order, and a CTA flushes its shared-memory histogram
+// before it starts any task that may block (T of another field, F) -- so the earliest
+// unfinished task can always run: no deadlock.  The value range of field f+1 (DRAM) and
+// the finalize of f-1 overlap the tiles of f (ALU), there is no launch or ramp between
+// fields, and field f arrives in L2 two phases before its tiles.  Histogram/partial
+// buffers rotate over f % 3 (T(f) waits fin_ready[f-3]).  All floating-point sums
+// are per task and reduced in task order: results are bit-identical to the per-field path.
+#include <vector>
+
+#include "sel_tile_common.cuh"
+
+namespace sel {
+
+constexpr int kFinTasks = 8;                   // F tasks per field (8192 slots each)
+constexpr int kRing = 3;                       // histogram / partial buffers (field % 3)
+constexpr int kLagT = 2, kLagF = 4;            // phase p: R(p), T(p - kLagT), F(p - kLagF)
+
+// float -> unsigned key with the same order (for atomicMin/atomicMax), and back
+__device__ __forceinline__ unsigned int float_key(float v) {
+  const unsigned int b = __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key_float(unsigned int k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+struct FPart { double acc, err; unsigned long long bits, ovf; };
+
+struct BatchArgs {
+  const CUtensorMap *tmaps;       // [nf], 64-B aligned, global
+  const float *const *xs;         // [nf] device pointers
+  int nf;
+  TileGeo tg;
+  int64_t N;
+  int nR, nT, phase;              // tasks per field (F: kFinTasks); phase = kFinTasks + nR + nT
+  int rchunk;                     // floats per R task
+  long long ntotal;               // (nf + 2) * phase
+  FinalizeArgs fa;
+  int mode;
+  double eb;
+  // state
+  Params *params;                 // [nf]
+  unsigned int *rmin, *rmax, *rbad; // [nf] order-preserving keys of min / max, non-finite flag
+  unsigned int *rdone;            // [nf] range slices done (nR * CW per field)
+  unsigned int *params_ready;     // [nf]
+  unsigned int *tdone;            // [nf] tile tasks whose histogram counts are flushed
+  unsigned int *fdone;            // [nf]
+  unsigned int *fin_ready;        // [nf]
+  unsigned long long *hist[kRing]; // per field f % kRing
+  Partial *tpart[kRing];          // [nT * CW]
+  FPart *fpart[kRing];            // [kFinTasks]
+  unsigned int *task_ctr;         // [1]
+  sel_result *results;            // [nf]
+};
+
+enum { KIND_NONE = 0, KIND_R = 1, KIND_T = 2, KIND_F = 3 };
+
+// Task sequence without padding.  Phase p holds F(p-kLagF) [kFinTasks] first, then
+// R(p) [nR] and T(p-kLagT) [nT] interleaved (Bresenham); absent fields contribute nothing.
+// R runs kLagT phases ahead of its tiles (its results are published at the next phase
+// boundary), F runs two phases after them (every CTA has flushed by then).
+__device__ __forceinline__ bool in_range(const BatchArgs &a, int f) { return f >= 0 && f < a.nf; }
+
+__device__ __forceinline__ long long phase_size(const BatchArgs &a, int p) {
+  return (long long)(in_range(a, p - kLagF) ? kFinTasks : 0) + (in_range(a, p) ? a.nR : 0) +
+         (in_range(a, p - kLagT) ? a.nT : 0);
+}
+
+__device__ __forceinline__ void decode(const BatchArgs &a, long long tau, int &kind, int &f, int &id,
+                                       int &phase) {
+  // phases 0 .. kLagF-1 are the ramp, kLagF .. nf-1 share one size, then the tail
+  int p = 0;
+  long long m = tau;
+  const int ramp_end = a.nf < kLagF ? a.nf : kLagF;
+  for (; p < ramp_end; ++p) {
+    const long long sz = phase_size(a, p);
+    if (m < sz) break;
+    m -= sz;
+  }
+  if (p == ramp_end) {
+    const int nmid = a.nf > kLagF ? a.nf - kLagF : 0;
+    const long long S = (long long)kFinTasks + a.nR + a.nT;
+    if (nmid > 0 && m < nmid * S) {
+      const int q = (int)(m / S);
+      p = kLagF + q;
+      m -= (long long)q * S;
+    } else {
+      m -= (long long)nmid * S;
+      p = ramp_end + nmid;
+      while (m >= phase_size(a, p)) { m -= phase_size(a, p); ++p; }
+    }
+  }
+  phase = p;
+  const int nF = in_range(a, p - kLagF) ? kFinTasks : 0;
+  if (m < nF) {
+    kind = KIND_F; f = p - kLagF; id = (int)m;
+    return;
+  }
+  m -= nF;
+  const long long nRp = in_range(a, p) ? a.nR : 0, nTp = in_range(a, p - kLagT) ? a.nT : 0;
+  const long long M = nRp + nTp;
+  const long long r0 = m * nRp / M, r1 = (m + 1) * nRp / M;
+  if (r1 > r0) { kind = KIND_R; f = p; id = (int)r0; }
+  else { kind = KIND_T; f = p - kLagT; id = (int)(m - r0); }
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// warp 0 lane 0 spins until *flag >= target (acquire); the caller syncs the consumers
+__device__ __forceinline__ void spin_until(const unsigned int *flag, unsigned int target) {
+  unsigned int ns = 32;
+  long long guard = 0;
+  while (ld_acquire(flag) < target) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+    if (++guard > (1LL << 24)) __trap();     // never hang the GPU on a logic error
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArgs a) {
+  using Cfg = TileCfg<D>;
+  constexpr int CW = Cfg::CW;
+  constexpr int NC = CW * 32;                  // consumer threads
+  extern __shared__ float smem_dyn[];
+  float *const base = smem_dyn + (((128u - (smem_u32(smem_dyn) & 127u)) & 127u) >> 2);
+  unsigned int *const hist = reinterpret_cast<unsigned int *>(base + Cfg::STAGES * Cfg::STAGE_FLOATS);
+  unsigned int *const tbl = hist + Cfg::HIST_WORDS;
+  // barriers + per-stage descriptors, 16-byte aligned (hist starts 128-byte aligned)
+  uint64_t *const full_bar =
+      reinterpret_cast<uint64_t *>(hist + ((Cfg::HIST_WORDS + Cfg::TBL_WORDS + 3) & ~3));
+  uint64_t *const empty_bar = full_bar + Cfg::STAGES;
+  // per stage, decoded once by the producer: {kind | end flag, f, id, phase} and the tile
+  // coordinates {btk, btj, bi}
+  int4 *const stage_desc = reinterpret_cast<int4 *>(empty_bar + Cfg::STAGES);
+  int4 *const stage_tile = stage_desc + Cfg::STAGES;
+  __shared__ double s_red[3][CW];
+  __shared__ unsigned long long s_redu[2][CW];
+  __shared__ Params s_prm;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], CW);
+    }
+    fence_barrier_init();
+  }
+  for (int i = tid; i < Cfg::HIST_WORDS + Cfg::TBL_WORDS; i += Cfg::THREADS) hist[i] = 0u;
+  __syncthreads();
+
+  // ------------------------------------------------------------------ producer
+  if (warp == CW) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (;;) {
+        const long long tau = (long long)atomicAdd(a.task_ctr, 1u);
+        mbar_wait(&empty_bar[stage], ph ^ 1u);
+        int kind = KIND_NONE, f = 0, id = 0, phase = 0;
+        if (tau < a.ntotal) decode(a, tau, kind, f, id, phase);
+        stage_desc[stage] = make_int4(tau >= a.ntotal ? -1 : kind, f, id, phase);
+        float *dst = base + stage * Cfg::STAGE_FLOATS;
+        if (kind == KIND_T) {
+          const int btk = id % a.tg.ntk;
+          const int rest = id / a.tg.ntk;
+          const int btj = rest % a.tg.ntj;
+          const int bi = rest / a.tg.ntj;
+          stage_tile[stage] = make_int4(btk, btj, bi, 0);
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          if constexpr (D == 3)
+            tma_load_3d(dst, a.tmaps + f, 128 * btk - 4, 4 * CW * btj - 1, 4 * bi - 1, &full_bar[stage]);
+          else
+            tma_load_2d(dst, a.tmaps + f, 128 * btk - 4, 4 * CW * btj - 1, &full_bar[stage]);
+        } else if (kind == KIND_R) {
+          const long long lo = (long long)id * a.rchunk;
+          const long long cnt = min((long long)a.rchunk, a.N - lo);   // multiple of 4 floats
+          mbar_arrive_expect_tx(&full_bar[stage], (uint32_t)(cnt * 4));
+          bulk_load(dst, a.xs[f] + lo, (uint32_t)(cnt * 4), &full_bar[stage]);
+        } else {
+          mbar_arrive(&full_bar[stage]);   // F / padding / sentinel: no data
+        }
+        if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
+        if (tau >= a.ntotal) break;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
+  unsigned int *const hlane = hist + (lane % Cfg::COPIES) * kHStride;
+  unsigned int *const htrash = hist + Cfg::COPIES * kHStride;
+  int cur = -1;                    // field owning the smem histogram
+  unsigned int cur_tasks = 0;      // its T tasks since the last flush
+  unsigned int ovf = 0;
+  bool ok = false;
+  float r_f = 0.f;
+  int minexp = 0;
+  DebugPtrs nodbg{};
+
+  auto flush = [&]() {             // all consumers, same task: move smem histogram to global
+    unsigned long long *gh = a.hist[cur % kRing];
+    ovf_flush(ovf, gh);
+    ovf = 0;
+    consumer_sync<NC>();
+    tile_hist_flush<D>(hist, tbl, gh, tid, NC);
+    __threadfence();
+    consumer_sync<NC>();
+    if (tid == 0) atomicAdd(a.tdone + cur, cur_tasks);
+    cur = -1;
+    cur_tasks = 0;
+  };
+
+  // this warp's range results not yet published (per field): published before any task
+  // that may block, so nobody can wait on them forever
+  int r_field = -1;
+  float r_mn = INFINITY, r_mx = -INFINITY;
+  int r_bad = 0;
+  unsigned int r_cnt = 0;
+  auto publish_range = [&]() {
+    if (r_field >= 0 && lane == 0) {
+      const int g = r_field;
+      if (r_mn <= r_mx) {
+        atomicMin(a.rmin + g, float_key(r_mn));
+        atomicMax(a.rmax + g, float_key(r_mx));
+      }
+      if (r_bad) atomicOr(a.rbad + g, 1u);
+      __threadfence();
+      if (atomicAdd(a.rdone + g, r_cnt) + r_cnt == (unsigned)a.nR * CW) {   // last: params(g)
+        __threadfence();
+        const float fmn = key_float(ld_acquire(a.rmin + g)), fmx = key_float(ld_acquire(a.rmax + g));
+        a.params[g] = make_params(fmn, fmx, (int)ld_acquire(a.rbad + g), a.mode, a.eb);
+        __threadfence();
+        st_release(a.params_ready + g, 1u);
+      }
+    }
+    __syncwarp();
+    r_field = -1;
+    r_mn = INFINITY;
+    r_mx = -INFINITY;
+    r_bad = 0;
+    r_cnt = 0;
+  };
+
+  int stage = 0;
+  uint32_t ph = 0;
+  for (;;) {
+    mbar_wait(&full_bar[stage], ph);
+    const int4 sd = stage_desc[stage];
+    const bool end = sd.x < 0;
+    const int kind = end ? KIND_NONE : sd.x, f = sd.y, id = sd.z, phase = sd.w;
+    // flush before anything that may block (another field's tiles wait on params /
+    // fin_ready, finalize waits on tdone) and at the end; range tasks never block
+    const bool may_block = end || kind == KIND_F || (kind == KIND_T && f != cur);
+    if (may_block || (r_field >= 0 && phase != r_field)) publish_range();   // R(p) is phase p
+    if (cur >= 0 && may_block) flush();
+    if (end) break;
+    const float *S = base + stage * Cfg::STAGE_FLOATS;
+
+    if (kind == KIND_T) {
+      if (cur < 0) {               // first tile of field f here: params, parity buffer free
+        if (tid == 0) {
+          spin_until(a.params_ready + f, 1u);
+          if (f >= kRing) spin_until(a.fin_ready + f - kRing, 1u);
+          s_prm = a.params[f];
+        }
+        consumer_sync<NC>();
+        const Params prm = s_prm;
+        ok = prm.status == SEL_OK;
+        r_f = prm.r_f;
+        minexp = prm.minexp;
+        cur = f;
+      }
+      uint64_t tbits = 0;
+      double terr = 0.0;
+      const int4 tc = stage_tile[stage];
+      tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hlane, htrash,
+                             tbl, a.hist[f % kRing], ovf, nodbg, tbits, terr);
+      ++cur_tasks;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      task_store(a.tpart[f % kRing], id * CW + warp, tbits, terr);
+    } else if (kind == KIND_R) {
+      // ---- min / max / non-finite over this warp's slice of the staged chunk (R1);
+      // order-preserving integer keys make the global combine a plain atomicMin/Max
+      const long long lo = (long long)id * a.rchunk;
+      const int n4 = (int)min((long long)a.rchunk, a.N - lo) / 4;
+      float mn = INFINITY, mx = -INFINITY;
+      int bad = 0;
+      for (int i = tid; i < n4; i += NC) {
+        const float4 q = reinterpret_cast<const float4 *>(S)[i];
+        bad |= is_nonfinite(q.x) | is_nonfinite(q.y) | is_nonfinite(q.z) | is_nonfinite(q.w);
+        mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
+        mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+      }
+      if (r_field != f) {          // first slice of f in this warp (publish any other field)
+        publish_range();
+        r_field = f;
+      }
+      r_mn = fminf(r_mn, mn);
+      r_mx = fmaxf(r_mx, mx);
+      r_bad |= bad;
+      ++r_cnt;
+    } else if (kind == KIND_F) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      if (tid == 0) spin_until(a.tdone + f, (unsigned)a.nT);
+      consumer_sync<NC>();
+      unsigned long long *gh = a.hist[f % kRing];
+      // ---- 1/8 of the histogram: sum c log2(N/c), re-zero; and 1/8 of the tile partials
+      const double Nsz = (double)a.fa.n_sz;
+      const double lN = log2(Nsz);
+      constexpr int PER = kNSlots / kFinTasks;
+      double acc = 0.0;
+      unsigned long long novf = 0;
+      for (int s = id * PER + tid; s < (id + 1) * PER; s += NC) {
+        const unsigned long long c = __ldcg(gh + s);
+        if (c) {
+          const double cd = (double)c;
+          acc += cd * (lN - log2(cd));
+          gh[s] = 0ull;
+        }
+        if (s == kOvfSlot) novf = c;
+      }
+      const int np = a.nT * CW;
+      const int per = (np + kFinTasks - 1) / kFinTasks;
+      const int p0 = id * per, p1 = min(p0 + per, np);
+      double err = 0.0;
+      unsigned long long bits = 0;
+      for (int t = p0 + tid; t < p1; t += NC) {
+        bits += __ldcg(&a.tpart[f % kRing][t].bits);
+        err += __ldcg(&a.tpart[f % kRing][t].err);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_down_sync(0xffffffffu, acc, o);
+        err += __shfl_down_sync(0xffffffffu, err, o);
+        bits += __shfl_down_sync(0xffffffffu, bits, o);
+        novf += __shfl_down_sync(0xffffffffu, novf, o);
+      }
+      consumer_sync<NC>();
+      if (lane == 0) { s_red[0][warp] = acc; s_red[1][warp] = err; s_redu[0][warp] = bits; s_redu[1][warp] = novf; }
+      consumer_sync<NC>();
+      if (tid == 0) {
+        for (int w = 1; w < CW; ++w) { acc += s_red[0][w]; err += s_red[1][w]; bits += s_redu[0][w]; novf += s_redu[1][w]; }
+        FPart fp;
+        fp.acc = acc; fp.err = err; fp.bits = bits; fp.ovf = novf;
+        a.fpart[f % kRing][id] = fp;
+        __threadfence();
+        if (atomicAdd(a.fdone + f, 1u) == (unsigned)kFinTasks - 1) {   // last: result f
+          __threadfence();
+          double S = 0.0, errs = 0.0;
+          unsigned long long tb = 0, ov = 0;
+          for (int k = 0; k < kFinTasks; ++k) {
+            S += __ldcg(&a.fpart[f % kRing][k].acc);
+            errs += __ldcg(&a.fpart[f % kRing][k].err);
+            tb += __ldcg(&a.fpart[f % kRing][k].bits);
+            ov += __ldcg(&a.fpart[f % kRing][k].ovf);
+          }
+          const Params prm = a.params[f];
+          const double mse = errs / (double)a.fa.n_values;
+          a.results[f] = assemble_result(prm, S, errs, tb, ov, a.fa, log10(prm.vr / prm.eb_abs),
+                                         log10(prm.vr), mse > 0.0 ? log10(mse) : 0.0);
+          __threadfence();
+          st_release(a.fin_ready + f, 1u);
+        }
+      }
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+    }
+    if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
+  }
+}
+
+// ============================================================ host side
+namespace {
+template <int D>
+const void *batch_fn() { return (const void *)k_batch<D>; }
+}  // namespace
+
+int batch_sizes(const Geo &g, BatchSizes *bs) {
+  const int d3 = g.ndims == 3;
+  bs->rchunk = d3 ? (TileCfg<3>::STAGE_FLOATS & ~3) : (TileCfg<2>::STAGE_FLOATS & ~3);
+  bs->nR = (int)((g.N + bs->rchunk - 1) / bs->rchunk);
+  bs->smem = d3 ? TileCfg<3>::SMEM : TileCfg<2>::SMEM;
+  bs->threads = d3 ? TileCfg<3>::THREADS : TileCfg<2>::THREADS;
+  bs->cw = d3 ? TileCfg<3>::CW : TileCfg<2>::CW;
+  const void *fn = d3 ? batch_fn<3>() : batch_fn<2>();
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs->smem) != cudaSuccess)
+    return SEL_ECUDA;
+  return SEL_OK;
+}
+
+size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT) {
+  return (size_t)nf * (sizeof(Params) + 8 * 4 + sizeof(CUtensorMap) + 8) +
+         kRing * ((size_t)kNSlots * 8 + (size_t)nT * bs.cw * sizeof(Partial) + kFinTasks * sizeof(FPart) + 768) +
+         4096;
+}
+
+int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
+                 int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
+                 sel_result *d_results, int sm_count, cudaStream_t st, cudaEvent_t *ev) {
+  // state layout (device): tmaps | xs | params | counters | hist x2 | tpart x2 | fpart x2
+  char *b = (char *)state;
+  size_t off = 0;
+  auto take = [&](size_t bytes, size_t align = 256) {
+    off = (off + align - 1) & ~(align - 1);
+    size_t o = off;
+    off += bytes;
+    return b + o;
+  };
+  const int nT = tl.tg.ntasks;
+  CUtensorMap *tmaps = (CUtensorMap *)take(sizeof(CUtensorMap) * nf, 128);
+  const float **xs = (const float **)take(sizeof(float *) * nf);
+  Params *params = (Params *)take(sizeof(Params) * nf);
+  unsigned int *ctrs = (unsigned int *)take(sizeof(unsigned int) * (8 * (size_t)nf + 1));
+  unsigned long long *hst[kRing];
+  Partial *tp[kRing];
+  FPart *fp[kRing];
+  for (int k = 0; k < kRing; ++k) {
+    hst[k] = (unsigned long long *)take((size_t)kNSlots * 8);
+    tp[k] = (Partial *)take(sizeof(Partial) * (size_t)nT * bs.cw);
+    fp[k] = (FPart *)take(sizeof(FPart) * kFinTasks);
+  }
+  if (off > state_bytes) return SEL_EINVAL;
+  // host-built tensor maps and pointer table, one H2D copy each (staged in pinned memory
+  // by the caller? small: a few KB -> plain cudaMemcpyAsync from pageable is fine)
+  static thread_local std::vector<CUtensorMap> h_maps;
+  h_maps.resize(nf);
+  for (int f = 0; f < nf; ++f)
+    if (make_tile_map(&h_maps[f], d_fields[f], g)) return SEL_ECUDA;
+  if (cudaMemcpyAsync(tmaps, h_maps.data(), sizeof(CUtensorMap) * nf, cudaMemcpyHostToDevice, st) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(xs, d_fields, sizeof(float *) * nf, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemsetAsync(ctrs, 0, sizeof(unsigned int) * (8 * (size_t)nf + 1), st) != cudaSuccess ||
+      cudaMemsetAsync(ctrs + 6 * (size_t)nf, 0xff, sizeof(unsigned int) * nf, st) != cudaSuccess ||
+      cudaMemsetAsync(hst[0], 0, (size_t)kNSlots * 8, st) != cudaSuccess ||
+      cudaMemsetAsync(hst[1], 0, (size_t)kNSlots * 8, st) != cudaSuccess ||
+      cudaMemsetAsync(hst[2], 0, (size_t)kNSlots * 8, st) != cudaSuccess)
+    return SEL_ECUDA;
+  BatchArgs a;
+  a.tmaps = tmaps;
+  a.xs = xs;
+  a.nf = nf;
+  a.tg = tl.tg;
+  a.N = g.N;
+  a.nR = bs.nR;
+  a.nT = nT;
+  a.phase = kFinTasks + bs.nR + nT;
+  a.rchunk = bs.rchunk;
+  a.ntotal = (long long)nf * (bs.nR + nT + kFinTasks);    // every real task exactly once
+  a.fa = fa;
+  a.mode = mode;
+  a.eb = eb;
+  a.params = params;
+  a.rdone = ctrs;
+  a.params_ready = ctrs + nf;
+  a.tdone = ctrs + 2 * nf;
+  a.fdone = ctrs + 3 * nf;
+  a.fin_ready = ctrs + 4 * nf;
+  a.rmax = ctrs + 5 * nf;
+  a.rmin = ctrs + 6 * nf;
+  a.rbad = ctrs + 7 * nf;
+  a.task_ctr = ctrs + 8 * nf;
+  for (int k = 0; k < kRing; ++k) {
+    a.hist[k] = hst[k];
+    a.tpart[k] = tp[k];
+    a.fpart[k] = fp[k];
+  }
+  a.results = d_results;
+  const void *fn = g.ndims == 3 ? batch_fn<3>() : batch_fn<2>();
+  void *args[] = {(void *)&a};
+  if (ev && cudaEventRecord(ev[0], st) != cudaSuccess) return SEL_ECUDA;
+  if (cudaLaunchKernel(fn, dim3(sm_count), dim3(bs.threads), args, bs.smem, st) != cudaSuccess)
+    return SEL_ECUDA;
+  if (ev && cudaEventRecord(ev[1], st) != cudaSuccess) return SEL_ECUDA;
+  return SEL_OK;
+}
+
+}  // namespace sel

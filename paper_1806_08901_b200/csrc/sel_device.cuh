@@ -272,6 +272,81 @@ __device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int mi
   E = __dmul_rn(s, pow2d(2 * (emax - 30)));
 }
 
+
+// Per-field result from the reduced sums (Eq. entropy, Eq. psnr-sz
+// P:410) and the Alg. 1 lines 7-10 selection (reading R16).
+// S = sum_s c_s log2(N/c_s); lg_* are log10(VR/eb), log10(VR), log10(MSE).
+__device__ __forceinline__ sel_result assemble_result(const Params &prm, double S, double errs,
+                                                      uint64_t tb, uint64_t novf,
+                                                      const FinalizeArgs &fa, double lg_vr_eb,
+                                                      double lg_vr, double lg_mse) {
+  sel_result r = {};
+  r.status = prm.status;
+  r.value_range = prm.vr;
+  r.eb_abs = prm.eb_abs;
+  r.minexp = prm.minexp;
+  r.r_f = prm.r_f;
+  r.n_sz_points = fa.n_sz;
+  r.n_values = fa.n_values;
+  r.n_blocks = fa.n_blocks;
+  if (r.status == SEL_OK && fa.n_sz == 0) r.status = SEL_EDEGENERATE;   // single-value field
+  if (r.status != SEL_OK) return r;
+  const double Nsz = (double)fa.n_sz;
+  const double vr = prm.vr, eb = prm.eb_abs;
+  const double mse = errs / (double)fa.n_values;
+  const double H = S / Nsz;
+  const double povf = (double)novf / Nsz;
+  r.sz_entropy = H;
+  r.sz_overflow_frac = povf;
+  r.sz_bits_per_value = H + fa.sz_offset + 32.0 * povf;
+  r.sz_psnr = 20.0 * lg_vr_eb + 10.0 * log10(3.0);
+  r.zfp_total_bits = tb;
+  r.zfp_err_sum = errs;
+  r.zfp_bits_per_value = (double)tb / (double)fa.n_values;
+  r.zfp_mse = mse;
+  r.zfp_psnr = mse > 0.0 ? 20.0 * lg_vr - 10.0 * lg_mse : __longlong_as_double(0x7ff0000000000000LL);
+  if (!(r.zfp_mse > 0.0) || !(vr > 0.0) || !isfinite(r.zfp_psnr)) {
+    r.matched = 0;
+    r.sz_bits_matched = r.sz_bits_per_value;
+    r.sz_eb_matched = eb;
+    r.choice = r.sz_bits_per_value < r.zfp_bits_per_value ? 0 : 1;
+  } else {
+    const double delta = vr * sqrt(12.0) * pow(10.0, -r.zfp_psnr / 20.0);
+    double bm = r.sz_bits_per_value + log2(2.0 * eb / delta);
+    if (bm < 0.0) bm = 0.0;
+    r.matched = 1;
+    r.sz_bits_matched = bm;
+    r.sz_eb_matched = delta / 2.0;
+    r.choice = bm < r.zfp_bits_per_value ? 0 : 1;
+  }
+  return r;
+}
+
+// value-range derived scalars (Alg. 1 line 2; readings R1, R2)
+__device__ __forceinline__ Params make_params(float mn, float mx, int bad, int mode, double eb) {
+  Params p;
+  p.vmin = mn; p.vmax = mx; p.pad = 0;
+  p.vr = (double)mx - (double)mn;
+  p.status = bad ? SEL_ENONFINITE : SEL_OK;
+  p.eb_abs = (mode == SEL_EB_REL) ? eb * p.vr : eb;
+  if (p.status == SEL_OK && mode == SEL_EB_REL && p.vr == 0.0) p.status = SEL_EDEGENERATE;
+  p.r_f = __double2float_rn(1.0 / (2.0 * p.eb_abs));
+  if (p.status == SEL_OK && (is_nonfinite(p.r_f) || !(p.eb_abs > 0.0))) p.status = SEL_EINVAL;
+  int e = 0;
+  frexp(p.eb_abs, &e);
+  p.minexp = e - 1;
+  return p;
+}
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // ============================================================ shared K2 prologue/epilogue
 __device__ __forceinline__ void hist_zero(unsigned int *sh) {
   uint4 *s4 = reinterpret_cast<uint4 *>(sh);

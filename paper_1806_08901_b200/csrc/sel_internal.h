@@ -123,7 +123,20 @@ int launch_minmax(const float *x, int64_t N, int ctas, const Workspace &ws, int 
 int plan_estimate(const Geo &g, int debug, int sm_count, EstLaunch *el);
 int launch_estimate(const float *x, const Geo &g, const EstLaunch &el, const Workspace &ws,
                     const DebugPtrs *dbg, cudaStream_t st);
+struct BatchSizes {
+  int rchunk;       // floats per value-range task
+  int nR;           // value-range tasks per field
+  size_t smem;
+  int threads;
+  int cw;           // consumer warps
+};
+
 bool tile_supported(const Geo &g);
+int batch_sizes(const Geo &g, BatchSizes *bs);
+size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT);
+int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
+                 int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
+                 sel_result *d_results, int sm_count, cudaStream_t st, cudaEvent_t *ev);
 int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl);
 int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Workspace &ws,
                 const DebugPtrs *dbg, cudaStream_t st);

@@ -119,17 +119,7 @@ __global__ void __launch_bounds__(THREADS) k_minmax(const float *__restrict__ x,
     for (int w = 1; w < THREADS / 32; ++w) {
       mn = fminf(mn, smn[w]); mx = fmaxf(mx, smx[w]); bad |= sbad[w];
     }
-    Params p;
-    p.vmin = mn; p.vmax = mx; p.pad = 0;
-    p.vr = (double)mx - (double)mn;                       // A1
-    p.status = bad ? SEL_ENONFINITE : SEL_OK;
-    p.eb_abs = (mode == SEL_EB_REL) ? eb * p.vr : eb;     // A2 (Alg.1 line 2)
-    if (p.status == SEL_OK && mode == SEL_EB_REL && p.vr == 0.0) p.status = SEL_EDEGENERATE;
-    p.r_f = __double2float_rn(1.0 / (2.0 * p.eb_abs));
-    if (p.status == SEL_OK && (is_nonfinite(p.r_f) || !(p.eb_abs > 0.0))) p.status = SEL_EINVAL;
-    int e = 0;
-    frexp(p.eb_abs, &e);
-    p.minexp = e - 1;                                     // floor(log2 eb_abs)
+    const Params p = make_params(mn, mx, bad, mode, eb);
     *ws.params = p;    // this field's own params slot
     ws.tickets[0] = 0;
   }
@@ -569,47 +559,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
   ws.tickets[1] = 0;
   *ws.task_ctr = 0;
 
-  sel_result r = {};
-  r.status = prm.status;
-  r.value_range = prm.vr;
-  r.eb_abs = prm.eb_abs;
-  r.minexp = prm.minexp;
-  r.r_f = prm.r_f;
-  r.n_sz_points = fa.n_sz;
-  r.n_values = fa.n_values;
-  r.n_blocks = fa.n_blocks;
-  if (r.status == SEL_OK && fa.n_sz == 0) r.status = SEL_EDEGENERATE;   // single-value field
-  if (r.status == SEL_OK) {
-    const double S = sfin[0] + sfin[2];
-    const uint64_t tb = sfb[0] + sfb[1];
-    const double H = S / Nsz;                                        // Eq. entropy
-    const double povf = (double)__ldcg(ws.fin_ovf) / Nsz;
-    r.sz_entropy = H;
-    r.sz_overflow_frac = povf;
-    r.sz_bits_per_value = H + fa.sz_offset + 32.0 * povf;            // P:402, R6
-    r.sz_psnr = 20.0 * slog[0] + 10.0 * log10(3.0);                  // Eq. psnr-sz
-    r.zfp_total_bits = tb;
-    r.zfp_err_sum = errs;
-    r.zfp_bits_per_value = (double)tb / (double)fa.n_values;
-    r.zfp_mse = mse;
-    r.zfp_psnr = mse > 0.0 ? 20.0 * slog[1] - 10.0 * slog[2]
-                           : __longlong_as_double(0x7ff0000000000000LL);
-    // Alg.1 lines 7-10 (R16)
-    if (!(r.zfp_mse > 0.0) || !(vr > 0.0) || !isfinite(r.zfp_psnr)) {
-      r.matched = 0;
-      r.sz_bits_matched = r.sz_bits_per_value;
-      r.sz_eb_matched = eb;
-      r.choice = r.sz_bits_per_value < r.zfp_bits_per_value ? 0 : 1;
-    } else {
-      const double delta = vr * sqrt(12.0) * pow(10.0, -r.zfp_psnr / 20.0);
-      double bm = r.sz_bits_per_value + log2(2.0 * eb / delta);
-      if (bm < 0.0) bm = 0.0;
-      r.matched = 1;
-      r.sz_bits_matched = bm;
-      r.sz_eb_matched = delta / 2.0;
-      r.choice = bm < r.zfp_bits_per_value ? 0 : 1;
-    }
-  }
+  const double S = sfin[0] + sfin[2];
+  const uint64_t tb = sfb[0] + sfb[1];
+  sel_result r = assemble_result(prm, S, errs, tb, __ldcg(ws.fin_ovf), fa, slog[0], slog[1], slog[2]);
   *out = r;
 }
 

@@ -188,33 +188,71 @@ def test_offset_option(sel, orc):
 # ---------------------------------------------------------------- batch APIs
 def test_batch_and_host_batch(sel, orc):
     import synth
-    shape = (60, 90)
+    shape = (60, 88)
     xs = [synth.c2_field(i, shape=shape) for i in range(5)]
     ts = [torch.from_numpy(x).cuda() for x in xs]
     hs = [torch.from_numpy(x).pin_memory() for x in xs]
     with sel.Plan(shape, 1e-4) as p:
         single = [p.estimate(t) for t in ts]
-        batch = p.estimate_batch(ts)
+        batch = p.estimate_batch(ts)                 # persistent k_batch (1 launch)
+        l0 = p.launch_count
+        p.estimate_batch(ts)
+        assert p.launch_count - l0 == 1
+        p.set_option("batch_kernel", 0)
+        piped = p.estimate_batch(ts)                 # 3-stream pipeline of per-field kernels
+        p.set_option("pipeline", 0)
+        seq = p.estimate_batch(ts)                   # plain sequential per-field kernels
         host = p.estimate_batch_host(hs)
         host_np = p.estimate_batch_host(xs)
-        assert p.launch_count == 3 * (5 + 5 + 5 + 5)
     for i, x in enumerate(xs):
         o = orc.estimate(x, 1e-4)
-        for r in (single[i], batch[i], host[i], host_np[i]):
+        for r in (single[i], batch[i], piped[i], seq[i], host[i], host_np[i]):
             compare_scalars(r, o, f"batch{i}")
+        for r in (piped[i], host[i]):
+            for k in seq[i]:
+                if isinstance(seq[i][k], float):
+                    assert close(r[k], seq[i][k], rel=1e-12), (i, k)
+                else:
+                    assert r[k] == seq[i][k], (i, k)
 
 
-def test_batch_reports_per_field_status(sel):
-    ts = [torch.ones(8, 8, device="cuda"), torch.arange(64, dtype=torch.float32, device="cuda").view(8, 8)]
+@pytest.mark.parametrize("batch_kernel", [1, 0])
+def test_batch_reports_per_field_status(sel, batch_kernel):
+    bad = torch.ones(8, 8, device="cuda")
+    nan = torch.arange(64, dtype=torch.float32, device="cuda").view(8, 8).clone()
+    nan[3, 3] = float("nan")
+    good = torch.arange(64, dtype=torch.float32, device="cuda").view(8, 8)
     with sel.Plan((8, 8), 1e-3) as p:
-        out = p.estimate_batch(ts)
+        p.set_option("batch_kernel", batch_kernel)
+        out = p.estimate_batch([bad, good, nan, good])
     assert out[0]["status"] == sel.SEL_EDEGENERATE and out[1]["status"] == 0
+    assert out[2]["status"] == sel.SEL_ENONFINITE and out[3]["status"] == 0
+    assert out[1]["choice"] == out[3]["choice"]
+
+
+@pytest.mark.parametrize("shape", [(96, 128), (20, 24, 36), (1, 1, 8)])
+def test_batch_kernel_many_fields(sel, orc, shape):
+    """k_batch over a longer stack (parity buffers reused, phases overlap) == oracle."""
+    rng = np.random.default_rng(sum(shape))
+    xs = [np.cumsum(rng.standard_normal(shape), axis=-1).astype(np.float32) * (i + 1) for i in range(9)]
+    ts = [torch.from_numpy(x).cuda() for x in xs]
+    with sel.Plan(shape, 1e-4) as p:
+        out = p.estimate_batch(ts)
+        again = p.estimate_batch(ts)
+    for i, x in enumerate(xs):
+        compare_scalars(out[i], orc.estimate(x, 1e-4), f"mf{i}")
+        assert out[i] == again[i]
 
 
 def test_kernel_timing_option(sel):
     t = torch.randn(256, 256, device="cuda")
     with sel.Plan(t.shape, 1e-4) as p:
         p.set_option("kernel_timing", 1)
+        for _ in range(3):
+            p.estimate(t)
+        ms, n = p.kernel_times(reset=True)
+        assert n[1] == 3 and ms[1] > 0              # k_batch counted as the fused pass
+        p.set_option("batch_kernel", 0)
         for _ in range(3):
             p.estimate(t)
         ms, n = p.kernel_times(reset=True)
