@@ -303,9 +303,16 @@ def main():
     # launch = 4 B x values in processed blocks
     nv = plan.processed_values
     dom = int(np.argmax(kms))
-    names = ["k_minmax", "k_tile" if min(st) == 1 and len(shape) > 1 and shape[-1] % 4 == 0 else "k_estimate",
-             "k_finalize"]
-    alg_bytes = {0: 4.0 * int(np.prod(shape)), 1: 4.0 * nv, 2: 65536 * 8.0}[dom]
+    batch_kernel = kcnt[0] == 0 and kcnt[2] == 0      # one k_batch launch per batch call
+    if batch_kernel:
+        # k_batch does the whole step (value range + tiles + finalize of every field):
+        # algorithmic bytes per launch = 4 B x all values of the stack
+        names = ["k_minmax", "k_batch", "k_finalize"]
+        alg_bytes = 4.0 * int(np.prod(shape)) * nf
+    else:
+        names = ["k_minmax", "k_tile" if min(st) == 1 and len(shape) > 1 and shape[-1] % 4 == 0
+                 else "k_estimate", "k_finalize"]
+        alg_bytes = {0: 4.0 * int(np.prod(shape)), 1: 4.0 * nv, 2: 65536 * 8.0}[dom]
     avg_ms = kms[dom] / max(kcnt[dom], 1)
     achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
     traffic = None
@@ -334,7 +341,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": names[dom],
                      "peak_source": peak_kind,
-                     "kernel_ms": {names[k]: kms[k] / max(kcnt[k], 1) for k in range(3)}},
+                     "kernel_ms": {names[k]: kms[k] / max(kcnt[k], 1) for k in range(3) if kcnt[k]},
+                     "alg_bytes_per_launch": alg_bytes},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

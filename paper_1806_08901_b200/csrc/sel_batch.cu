@@ -27,6 +27,17 @@ namespace sel {
 constexpr int kFinTasks = 8;                   // F tasks per field (8192 slots each)
 constexpr int kRing = 3;                       // histogram / partial buffers (field % 3)
 constexpr int kLagT = 2, kLagF = 4;            // phase p: R(p), T(p - kLagT), F(p - kLagF)
+constexpr int kRWarps = 2;                     // consumer warps reducing one range chunk
+#ifndef SEL_BATCH_PROF
+#define SEL_BATCH_PROF 0                       // 1: per-CTA cycle counters (sel_dev_batch_profile)
+#endif
+#if SEL_BATCH_PROF
+#define PROF(stmt) stmt
+#define PCLOCK() clock64()
+#else
+#define PROF(stmt)
+#define PCLOCK() 0LL
+#endif
 
 // float -> unsigned key with the same order (for atomicMin/atomicMax), and back
 __device__ __forceinline__ unsigned int float_key(float v) {
@@ -63,6 +74,7 @@ struct BatchArgs {
   FPart *fpart[kRing];            // [kFinTasks]
   unsigned int *task_ctr;         // [1]
   sel_result *results;            // [nf]
+  unsigned long long *prof;       // optional [gridDim * 8] cycle counters (warp 0 of each CTA)
 };
 
 enum { KIND_NONE = 0, KIND_R = 1, KIND_T = 2, KIND_F = 3 };
@@ -116,13 +128,33 @@ __device__ __forceinline__ void decode(const BatchArgs &a, long long tau, int &k
   else { kind = KIND_T; f = p - kLagT; id = (int)(m - r0); }
 }
 
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                          uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_hint(void *dst, const CUtensorMap *map, int c0, int c1,
+                                                 int c2, uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *map, int c0, int c1,
+                                                 uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // warp 0 lane 0 spins until *flag >= target (acquire); the caller syncs the consumers
 __device__ __forceinline__ void spin_until(const unsigned int *flag, unsigned int target) {
@@ -155,9 +187,15 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   __shared__ double s_red[3][CW];
   __shared__ unsigned long long s_redu[2][CW];
   __shared__ Params s_prm;
+  __shared__ int s_tbl_used;
+  __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2], s_rpass[2];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   if (tid == 0) {
+    s_tbl_used = 0;
+    for (int k = 0; k < 2; ++k) {
+      s_rmin[k] = 0xffffffffu; s_rmax[k] = 0u; s_rbad[k] = 0u; s_rcnt[k] = 0u; s_rpass[k] = 0u;
+    }
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], CW);
@@ -172,8 +210,17 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
     if (lane == 0) {
       int stage = 0;
       uint32_t ph = 0;
+      // L2 policies: a range task's chunk is read again by the field's tiles two phases
+      // later (keep it: evict_last); a tile is the last use (evict_first)
+      uint64_t pol_keep, pol_last;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_last));
+      // the next task id is fetched one task ahead, so the atomic's round trip overlaps
+      // the wait for a free stage
+      long long next = (long long)atomicAdd(a.task_ctr, 1u);
       for (;;) {
-        const long long tau = (long long)atomicAdd(a.task_ctr, 1u);
+        const long long tau = next;
+        if (tau < a.ntotal) next = (long long)atomicAdd(a.task_ctr, 1u);
         mbar_wait(&empty_bar[stage], ph ^ 1u);
         int kind = KIND_NONE, f = 0, id = 0, phase = 0;
         if (tau < a.ntotal) decode(a, tau, kind, f, id, phase);
@@ -187,14 +234,16 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
           stage_tile[stage] = make_int4(btk, btj, bi, 0);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
-            tma_load_3d(dst, a.tmaps + f, 128 * btk - 4, 4 * CW * btj - 1, 4 * bi - 1, &full_bar[stage]);
+            tma_load_3d_hint(dst, a.tmaps + f, 128 * btk - 4, 4 * CW * btj - 1, 4 * bi - 1,
+                             &full_bar[stage], pol_last);
           else
-            tma_load_2d(dst, a.tmaps + f, 128 * btk - 4, 4 * CW * btj - 1, &full_bar[stage]);
+            tma_load_2d_hint(dst, a.tmaps + f, 128 * btk - 4, 4 * CW * btj - 1, &full_bar[stage],
+                             pol_last);
         } else if (kind == KIND_R) {
           const long long lo = (long long)id * a.rchunk;
           const long long cnt = min((long long)a.rchunk, a.N - lo);   // multiple of 4 floats
           mbar_arrive_expect_tx(&full_bar[stage], (uint32_t)(cnt * 4));
-          bulk_load(dst, a.xs[f] + lo, (uint32_t)(cnt * 4), &full_bar[stage]);
+          bulk_load(dst, a.xs[f] + lo, (uint32_t)(cnt * 4), &full_bar[stage], pol_keep);
         } else {
           mbar_arrive(&full_bar[stage]);   // F / padding / sentinel: no data
         }
@@ -216,62 +265,120 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   int minexp = 0;
   DebugPtrs nodbg{};
 
+#if SEL_BATCH_PROF
+  long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // wait, flush, T, R, F, release, #flush, #publish
+#endif
+
+  // Releases are deferred: a flush / publish issues its atomics and the counter increment
+  // that makes them visible (fence + add) happens at the next task boundary, when the
+  // atomics have drained, so the fence is cheap.  Every task boundary runs the pending
+  // releases BEFORE any wait, so nobody can wait on an unreleased contribution.
+  int pend_t_field = -1;           // tid 0: tdone[pend_t_field] += pend_t_cnt pending
+  unsigned int pend_t_cnt = 0;
+  int pend_r_field = -1;           // lane 0 of a publishing warp: rdone[field] += pend_r_cnt
+  unsigned int pend_r_cnt = 0;
+  auto release = [&]() {
+    const long long tp0 = PCLOCK();
+    if (tid == 0 && pend_t_field >= 0) {
+      fence_acq_rel_gpu();
+      atomicAdd(a.tdone + pend_t_field, pend_t_cnt);
+      pend_t_field = -1;
+    }
+    if (lane == 0 && pend_r_field >= 0) {
+      const int g = pend_r_field;
+      fence_acq_rel_gpu();
+      if (atomicAdd(a.rdone + g, pend_r_cnt) + pend_r_cnt == (unsigned)a.nR * kRWarps) {   // last
+
+        fence_acq_rel_gpu();
+        const float fmn = key_float(ld_acquire(a.rmin + g)), fmx = key_float(ld_acquire(a.rmax + g));
+        a.params[g] = make_params(fmn, fmx, (int)ld_acquire(a.rbad + g), a.mode, a.eb);
+        fence_acq_rel_gpu();
+        st_release(a.params_ready + g, 1u);
+      }
+      pend_r_field = -1;
+    }
+    PROF(pc[5] += clock64() - tp0);
+  };
+
   auto flush = [&]() {             // all consumers, same task: move smem histogram to global
     unsigned long long *gh = a.hist[cur % kRing];
+    const long long q0 = PCLOCK();
     ovf_flush(ovf, gh);
     ovf = 0;
+    const long long q1 = PCLOCK();
     consumer_sync<NC>();
-    tile_hist_flush<D>(hist, tbl, gh, tid, NC);
-    __threadfence();
-    consumer_sync<NC>();
-    if (tid == 0) atomicAdd(a.tdone + cur, cur_tasks);
+    const long long q2 = PCLOCK();
+    PROF(pc[6] += 1);
+    tile_hist_flush<D>(hist, tbl, &s_tbl_used, gh, tid, NC);
+    const long long q3 = PCLOCK();
+    consumer_sync<NC>();           // every consumer's atomics issued before the release
+    const long long q4 = PCLOCK();
+    if (SEL_BATCH_PROF && a.prof && tid == 0) {
+      atomicAdd(a.prof + 148 * 8 + 0, (unsigned long long)(q1 - q0));
+      atomicAdd(a.prof + 148 * 8 + 1, (unsigned long long)(q2 - q1));
+      atomicAdd(a.prof + 148 * 8 + 2, (unsigned long long)(q3 - q2));
+      atomicAdd(a.prof + 148 * 8 + 3, (unsigned long long)(q4 - q3));
+    }
+    if (tid == 0) {
+      s_tbl_used = 0;
+      pend_t_field = cur;
+      pend_t_cnt = cur_tasks;
+    }
     cur = -1;
     cur_tasks = 0;
   };
 
-  // this warp's range results not yet published (per field): published before any task
-  // that may block, so nobody can wait on them forever
-  int r_field = -1;
-  float r_mn = INFINITY, r_mx = -INFINITY;
-  int r_bad = 0;
-  unsigned int r_cnt = 0;
-  auto publish_range = [&]() {
-    if (r_field >= 0 && lane == 0) {
-      const int g = r_field;
-      if (r_mn <= r_mx) {
-        atomicMin(a.rmin + g, float_key(r_mn));
-        atomicMax(a.rmax + g, float_key(r_mx));
-      }
-      if (r_bad) atomicOr(a.rbad + g, 1u);
-      __threadfence();
-      if (atomicAdd(a.rdone + g, r_cnt) + r_cnt == (unsigned)a.nR * CW) {   // last: params(g)
-        __threadfence();
-        const float fmn = key_float(ld_acquire(a.rmin + g)), fmx = key_float(ld_acquire(a.rmax + g));
-        a.params[g] = make_params(fmn, fmx, (int)ld_acquire(a.rbad + g), a.mode, a.eb);
-        __threadfence();
-        st_release(a.params_ready + g, 1u);
+  // Range results are accumulated per CTA in shared memory (slot = phase parity) and
+  // published by the last consumer warp of the CTA to leave the phase (every consumer
+  // warp walks the same task sequence, so every warp sees every phase change).
+  int cur_phase = 0;
+  auto leave_phase = [&]() {
+    if (lane == 0) {
+      const int pp = cur_phase & 1;
+      if (atomicAdd(&s_rpass[pp], 1u) == (unsigned)CW - 1) {     // last warp out of the phase
+        const unsigned int cnt = s_rcnt[pp];
+        if (cnt) {
+          const int g = cur_phase;                                // R(p) belongs to field p
+          if (s_rmin[pp] != 0xffffffffu) atomicMin(a.rmin + g, s_rmin[pp]);
+          if (s_rmax[pp] != 0u) atomicMax(a.rmax + g, s_rmax[pp]);
+          if (s_rbad[pp]) atomicOr(a.rbad + g, 1u);
+          pend_r_field = g;
+          pend_r_cnt = cnt;
+          PROF(pc[7] += 1);
+        }
+        s_rmin[pp] = 0xffffffffu;
+        s_rmax[pp] = 0u;
+        s_rbad[pp] = 0u;
+        s_rcnt[pp] = 0u;
+        s_rpass[pp] = 0u;
       }
     }
     __syncwarp();
-    r_field = -1;
-    r_mn = INFINITY;
-    r_mx = -INFINITY;
-    r_bad = 0;
-    r_cnt = 0;
   };
 
   int stage = 0;
   uint32_t ph = 0;
   for (;;) {
+    const long long t_w0 = PCLOCK();
     mbar_wait(&full_bar[stage], ph);
+    const long long t_w1 = PCLOCK();
+    PROF(pc[0] += t_w1 - t_w0);      // waiting for data
     const int4 sd = stage_desc[stage];
     const bool end = sd.x < 0;
     const int kind = end ? KIND_NONE : sd.x, f = sd.y, id = sd.z, phase = sd.w;
     // flush before anything that may block (another field's tiles wait on params /
     // fin_ready, finalize waits on tdone) and at the end; range tasks never block
     const bool may_block = end || kind == KIND_F || (kind == KIND_T && f != cur);
-    if (may_block || (r_field >= 0 && phase != r_field)) publish_range();   // R(p) is phase p
+    release();                     // last boundary's flush / publish (their atomics drained)
+    while (cur_phase < (end ? a.nf + kLagF + 1 : phase)) {       // phase change(s)
+      leave_phase();
+      ++cur_phase;
+      if (end) release();          // several publishes in a row at the end
+    }
     if (cur >= 0 && may_block) flush();
+    if (may_block) release();      // about to wait: nothing of ours may stay unreleased
+    const long long t_k0 = PCLOCK();
+    PROF(pc[1] += t_k0 - t_w1);      // publish + flush
     if (end) break;
     const float *S = base + stage * Cfg::STAGE_FLOATS;
 
@@ -293,40 +400,49 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       double terr = 0.0;
       const int4 tc = stage_tile[stage];
       tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hlane, htrash,
-                             tbl, a.hist[f % kRing], ovf, nodbg, tbits, terr);
+                             tbl, &s_tbl_used, a.hist[f % kRing], ovf, nodbg, tbits, terr);
       ++cur_tasks;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
       task_store(a.tpart[f % kRing], id * CW + warp, tbits, terr);
     } else if (kind == KIND_R) {
-      // ---- min / max / non-finite over this warp's slice of the staged chunk (R1);
-      // order-preserving integer keys make the global combine a plain atomicMin/Max
-      const long long lo = (long long)id * a.rchunk;
-      const int n4 = (int)min((long long)a.rchunk, a.N - lo) / 4;
-      float mn = INFINITY, mx = -INFINITY;
-      int bad = 0;
-      for (int i = tid; i < n4; i += NC) {
-        const float4 q = reinterpret_cast<const float4 *>(S)[i];
-        bad |= is_nonfinite(q.x) | is_nonfinite(q.y) | is_nonfinite(q.z) | is_nonfinite(q.w);
-        mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
-        mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      // ---- min / max / non-finite of the staged chunk (R1) by kRWarps consumer warps
+      // (rotating with the task id); the others release the stage at once and move on.
+      // Order-preserving integer keys make the combines plain atomicMin/Max.
+      const int slot = (warp - (id * kRWarps) % CW + CW) % CW;
+      if (slot >= kRWarps) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      } else {
+        const long long lo = (long long)id * a.rchunk;
+        const int n4 = (int)min((long long)a.rchunk, a.N - lo) / 4;
+        float mn = INFINITY, mx = -INFINITY;
+        int bad = 0;
+#pragma unroll 4
+        for (int i = slot * 32 + lane; i < n4; i += kRWarps * 32) {
+          const float4 q = reinterpret_cast<const float4 *>(S)[i];
+          bad |= is_nonfinite(q.x) | is_nonfinite(q.y) | is_nonfinite(q.z) | is_nonfinite(q.w);
+          mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
+          mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[stage]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        for (int o = 16; o > 0; o >>= 1) {
+          mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        }
+        if (lane == 0) {
+          const int pp = phase & 1;
+          if (mn <= mx) {
+            atomicMin(&s_rmin[pp], float_key(mn));
+            atomicMax(&s_rmax[pp], float_key(mx));
+          }
+          if (bad) atomicOr(&s_rbad[pp], 1u);
+          atomicAdd(&s_rcnt[pp], 1u);
+        }
       }
-      if (r_field != f) {          // first slice of f in this warp (publish any other field)
-        publish_range();
-        r_field = f;
-      }
-      r_mn = fminf(r_mn, mn);
-      r_mx = fmaxf(r_mx, mx);
-      r_bad |= bad;
-      ++r_cnt;
     } else if (kind == KIND_F) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
@@ -372,9 +488,9 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
         FPart fp;
         fp.acc = acc; fp.err = err; fp.bits = bits; fp.ovf = novf;
         a.fpart[f % kRing][id] = fp;
-        __threadfence();
+        fence_acq_rel_gpu();
         if (atomicAdd(a.fdone + f, 1u) == (unsigned)kFinTasks - 1) {   // last: result f
-          __threadfence();
+          fence_acq_rel_gpu();
           double S = 0.0, errs = 0.0;
           unsigned long long tb = 0, ov = 0;
           for (int k = 0; k < kFinTasks; ++k) {
@@ -387,7 +503,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
           const double mse = errs / (double)a.fa.n_values;
           a.results[f] = assemble_result(prm, S, errs, tb, ov, a.fa, log10(prm.vr / prm.eb_abs),
                                          log10(prm.vr), mse > 0.0 ? log10(mse) : 0.0);
-          __threadfence();
+          fence_acq_rel_gpu();
           st_release(a.fin_ready + f, 1u);
         }
       }
@@ -395,11 +511,24 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
     }
+#if SEL_BATCH_PROF
+    {
+      const long long dt = clock64() - t_k0;
+      if (kind == KIND_T) pc[2] += dt;
+      else if (kind == KIND_R) pc[3] += dt;
+      else pc[4] += dt;
+    }
+#endif
     if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
   }
+#if SEL_BATCH_PROF
+  if (a.prof && tid == 0)
+    for (int k = 0; k < 8; ++k) a.prof[blockIdx.x * 8 + k] = (unsigned long long)pc[k];
+#endif
 }
 
 // ============================================================ host side
+unsigned long long *g_batch_prof = nullptr;   // developer profiling hook (sel_batch_profile)
 namespace {
 template <int D>
 const void *batch_fn() { return (const void *)k_batch<D>; }
@@ -495,6 +624,7 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
     a.fpart[k] = fp[k];
   }
   a.results = d_results;
+  a.prof = g_batch_prof;
   const void *fn = g.ndims == 3 ? batch_fn<3>() : batch_fn<2>();
   void *args[] = {(void *)&a};
   if (ev && cudaEventRecord(ev[0], st) != cudaSuccess) return SEL_ECUDA;
@@ -505,3 +635,7 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
 }
 
 }  // namespace sel
+
+// Developer hook (not part of include/sel.h): per-CTA cycle counters of k_batch's warp 0
+// {data wait, publish+flush, T, R, F, other} into dev_buf[ctas * 8]; NULL disables.
+extern "C" void sel_dev_batch_profile(unsigned long long *dev_buf) { sel::g_batch_prof = dev_buf; }

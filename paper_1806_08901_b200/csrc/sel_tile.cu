@@ -35,8 +35,10 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
   uint64_t *const empty_bar = full_bar + Cfg::STAGES;
   int4 *const stage_task = reinterpret_cast<int4 *>(empty_bar + Cfg::STAGES);   // {t, btk, btj, bi}
 
+  __shared__ int s_tbl_used;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    s_tbl_used = 0;
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], CW);
@@ -54,8 +56,10 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       int stage = 0;
       uint32_t ph = 0;
+      int next = (int)atomicAdd(ws.task_ctr, 1u);     // fetched one task ahead
       for (;;) {
-        const int t = (int)atomicAdd(ws.task_ctr, 1u);
+        const int t = next;
+        if (t < tg.ntasks) next = (int)atomicAdd(ws.task_ctr, 1u);
         mbar_wait(&empty_bar[stage], ph ^ 1u);
         if (t >= tg.ntasks) {           // sentinel stage: consumers stop here
           stage_task[stage] = make_int4(t, 0, 0, 0);
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
     uint64_t tbits = 0;
     double terr = 0.0;
     tile_consume<D, DBG>(S, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hlane, htrash, tbl,
-                         ws.hist, ovf, dbg, tbits, terr);
+                         &s_tbl_used, ws.hist, ovf, dbg, tbits, terr);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[stage]);      // stage free for the producer
     task_store(ws.task_part, t * CW + warp, tbits, terr);
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
   }
   ovf_flush(ovf, ws.hist);
   consumer_sync<CW * 32>();
-  tile_hist_flush<D>(hist, tbl, ws.hist, threadIdx.x, CW * 32);
+  tile_hist_flush<D>(hist, tbl, &s_tbl_used, ws.hist, threadIdx.x, CW * 32);
 }
 
 // ============================================================ host side

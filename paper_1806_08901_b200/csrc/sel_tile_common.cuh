@@ -122,7 +122,8 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
                                              const TileGeo &tg, int warp,
                                              int lane, bool ok, float r_f, int minexp,
                                              unsigned int *hlane, unsigned int *htrash,
-                                             unsigned int *tbl, unsigned long long *ghist,
+                                             unsigned int *tbl, int *tbl_used,
+                                             unsigned long long *ghist,
                                              unsigned int &ovf, const DebugPtrs &dbg,
                                              uint64_t &tbits, double &terr) {
   using Cfg = TileCfg<D>;
@@ -214,6 +215,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
                   if (sl > 65534u) {
                     ++ovf;
                   } else if (tb < (uint32_t)Cfg::TB) {
+                    *tbl_used = 1;
                     // packed 16-bit counter; the increment that takes it to 0x8000 moves
                     // 0x8000 counts to the global histogram, so it never carries
                     const uint32_t sh = (tb & 1u) << 4;
@@ -268,7 +270,8 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
 // and clear it.  Called by the consumer threads (tid < nthr) after a consumer barrier.
 template <int D>
 __device__ __forceinline__ void tile_hist_flush(unsigned int *hist, unsigned int *tbl,
-                                                unsigned long long *ghist, int tid, int nthr) {
+                                                const int *tbl_used, unsigned long long *ghist,
+                                                int tid, int nthr) {
   using Cfg = TileCfg<D>;
   for (int i = tid; i < kHBins; i += nthr) {
     unsigned long long c = 0;
@@ -279,6 +282,7 @@ __device__ __forceinline__ void tile_hist_flush(unsigned int *hist, unsigned int
     }
     if (c) atomicAdd(ghist + (kCenter - kHBins / 2) + i, c);
   }
+  if (!*tbl_used) return;               // no code outside the lane-copy window: table is zero
   for (int i = tid; i < Cfg::TBL_WORDS; i += nthr) {
     const uint32_t v = tbl[i];
     tbl[i] = 0u;

@@ -44,6 +44,22 @@ for i, f in enumerate(fields[:10]):
     for _ in range(3):
         r = p.estimate(f)
     ms, n = p.kernel_times(reset=True)
-    rows.append((i, [round(m / c * 1000, 1) for m, c in zip(ms, n)], round(r["sz_entropy"], 2), r["choice"]))
+    rows.append((i, [round(m / max(c, 1) * 1000, 1) for m, c in zip(ms, n)], round(r["sz_entropy"], 2), r["choice"]))
 for row in rows:
     print("field", *row)
+# k_batch per-phase cycle breakdown (warp 0 of each CTA)
+import ctypes
+buf = torch.zeros(148 * 8 + 8, dtype=torch.int64, device="cuda")
+sel.lib().sel_dev_batch_profile(ctypes.c_void_p(buf.data_ptr()))
+p.set_option("kernel_timing", 0)
+p.estimate_batch(fields)
+torch.cuda.synchronize()
+v = buf[:148 * 8].view(148, 8).double().cpu().numpy()
+q = buf[148 * 8:].double().cpu().numpy() / 148
+print("flush parts per CTA (ovf, bar1, hist, bar2):", [f"{x/1e3:.1f}k" for x in q[:4]])
+names = ["wait", "flush+publish", "T", "R", "F", "release"]
+tot = v[:, :6].sum(1)
+print("k_batch warp-0 cycles per CTA (mean):", {n: f"{v[:, k].mean()/1e3:.1f}k ({v[:, k].mean()/tot.mean()*100:.0f}%)" for k, n in enumerate(names)})
+print("flushes per CTA %.1f, publishes per warp0 %.1f" % (v[:, 6].mean(), v[:, 7].mean()))
+print("CTA total spread: min %.1fk max %.1fk" % (tot.min()/1e3, tot.max()/1e3))
+sel.lib().sel_dev_batch_profile(None)
