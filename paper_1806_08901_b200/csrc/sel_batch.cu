@@ -37,6 +37,7 @@ constexpr int kRWarps = 2;                     // consumer warps reducing one ra
 #else
 #define PROF(stmt)
 #define PCLOCK() 0LL
+#pragma nv_diag_suppress 177                    // timestamps unused without profiling
 #endif
 
 // float -> unsigned key with the same order (for atomicMin/atomicMax), and back
@@ -188,13 +189,13 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   __shared__ unsigned long long s_redu[2][CW];
   __shared__ Params s_prm;
   __shared__ int s_tbl_used;
-  __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2], s_rpass[2];
+  __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   if (tid == 0) {
     s_tbl_used = 0;
     for (int k = 0; k < 2; ++k) {
-      s_rmin[k] = 0xffffffffu; s_rmax[k] = 0u; s_rbad[k] = 0u; s_rcnt[k] = 0u; s_rpass[k] = 0u;
+      s_rmin[k] = 0xffffffffu; s_rmax[k] = 0u; s_rbad[k] = 0u; s_rcnt[k] = 0u;
     }
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   // releases BEFORE any wait, so nobody can wait on an unreleased contribution.
   int pend_t_field = -1;           // tid 0: tdone[pend_t_field] += pend_t_cnt pending
   unsigned int pend_t_cnt = 0;
-  int pend_r_field = -1;           // lane 0 of a publishing warp: rdone[field] += pend_r_cnt
+  int pend_r_field = -1;           // tid 0: rdone[field] += pend_r_cnt pending
   unsigned int pend_r_cnt = 0;
   auto release = [&]() {
     const long long tp0 = PCLOCK();
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       atomicAdd(a.tdone + pend_t_field, pend_t_cnt);
       pend_t_field = -1;
     }
-    if (lane == 0 && pend_r_field >= 0) {
+    if (tid == 0 && pend_r_field >= 0) {
       const int g = pend_r_field;
       fence_acq_rel_gpu();
       if (atomicAdd(a.rdone + g, pend_r_cnt) + pend_r_cnt == (unsigned)a.nR * kRWarps) {   // last
@@ -328,32 +329,31 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
     cur_tasks = 0;
   };
 
-  // Range results are accumulated per CTA in shared memory (slot = phase parity) and
-  // published by the last consumer warp of the CTA to leave the phase (every consumer
-  // warp walks the same task sequence, so every warp sees every phase change).
+  // Range results are accumulated per CTA in shared memory (slot = phase parity).  At a
+  // phase change every consumer warp meets at a barrier (they all walk the same task
+  // sequence, so they all see the change at the same task); after it, every range slice
+  // of the phase is in the slot and tid 0 publishes it.  Warps can then only move one
+  // phase ahead (into the other slot) before the next such barrier.
   int cur_phase = 0;
   auto leave_phase = [&]() {
-    if (lane == 0) {
+    consumer_sync<NC>();
+    if (tid == 0) {
       const int pp = cur_phase & 1;
-      if (atomicAdd(&s_rpass[pp], 1u) == (unsigned)CW - 1) {     // last warp out of the phase
-        const unsigned int cnt = s_rcnt[pp];
-        if (cnt) {
-          const int g = cur_phase;                                // R(p) belongs to field p
-          if (s_rmin[pp] != 0xffffffffu) atomicMin(a.rmin + g, s_rmin[pp]);
-          if (s_rmax[pp] != 0u) atomicMax(a.rmax + g, s_rmax[pp]);
-          if (s_rbad[pp]) atomicOr(a.rbad + g, 1u);
-          pend_r_field = g;
-          pend_r_cnt = cnt;
-          PROF(pc[7] += 1);
-        }
-        s_rmin[pp] = 0xffffffffu;
-        s_rmax[pp] = 0u;
-        s_rbad[pp] = 0u;
-        s_rcnt[pp] = 0u;
-        s_rpass[pp] = 0u;
+      const unsigned int cnt = s_rcnt[pp];
+      if (cnt) {
+        const int g = cur_phase;                                  // R(p) belongs to field p
+        if (s_rmin[pp] != 0xffffffffu) atomicMin(a.rmin + g, s_rmin[pp]);
+        if (s_rmax[pp] != 0u) atomicMax(a.rmax + g, s_rmax[pp]);
+        if (s_rbad[pp]) atomicOr(a.rbad + g, 1u);
+        pend_r_field = g;
+        pend_r_cnt = cnt;
+        PROF(pc[7] += 1);
       }
+      s_rmin[pp] = 0xffffffffu;
+      s_rmax[pp] = 0u;
+      s_rbad[pp] = 0u;
+      s_rcnt[pp] = 0u;
     }
-    __syncwarp();
   };
 
   int stage = 0;
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
     while (cur_phase < (end ? a.nf + kLagF + 1 : phase)) {       // phase change(s)
       leave_phase();
       ++cur_phase;
-      if (end) release();          // several publishes in a row at the end
+      release();                   // several phase changes in a row (empty phases, the end)
     }
     if (cur >= 0 && may_block) flush();
     if (may_block) release();      // about to wait: nothing of ours may stay unreleased

@@ -230,6 +230,21 @@ def test_batch_reports_per_field_status(sel, batch_kernel):
     assert out[1]["choice"] == out[3]["choice"]
 
 
+@pytest.mark.parametrize("nf", [1, 2, 3, 4, 5, 7])
+@pytest.mark.parametrize("shape", [(8, 12), (4, 4, 8), (3, 5, 4), (1, 4)])
+def test_batch_kernel_tiny_stacks(sel, orc, nf, shape):
+    """Stacks of tiny fields: most CTAs get no task, phases are empty or shorter than
+    the stage ring -- the task dataflow must neither deadlock nor mix fields."""
+    rng = np.random.default_rng(nf * 100 + sum(shape))
+    xs = [(rng.standard_normal(shape) * (i + 1)).astype(np.float32) for i in range(nf)]
+    xs[0] = np.cumsum(xs[0].ravel()).reshape(shape).astype(np.float32)
+    ts = [torch.from_numpy(x).cuda() for x in xs]
+    with sel.Plan(shape, 1e-3) as p:
+        out = p.estimate_batch(ts)
+    for i, x in enumerate(xs):
+        compare_scalars(out[i], orc.estimate(x, 1e-3), f"tiny{nf}/{i}")
+
+
 @pytest.mark.parametrize("shape", [(96, 128), (20, 24, 36), (1, 1, 8)])
 def test_batch_kernel_many_fields(sel, orc, shape):
     """k_batch over a longer stack (parity buffers reused, phases overlap) == oracle."""
