@@ -112,6 +112,18 @@ int sel_estimate(sel_plan_t plan, const float *d_field, void *stream, sel_result
 int sel_estimate_batch(sel_plan_t plan, const float *const *d_fields, int n, void *stream,
                        sel_result *out);
 
+/* Stream-ordered variant of sel_estimate_batch: enqueues the estimate of the n fields
+ * and a copy of the n results to `out` on `stream` and returns without waiting.
+ *   out : DEVICE memory or page-locked HOST memory (cudaHostAlloc / pinned), room for n
+ *         sel_result; valid once `stream` has been synchronised (caller's job).
+ * The plan's workspace is reused by its next call, so successive calls on one plan must
+ * be issued to the same stream (or ordered by the caller).  Not available while the
+ * options debug or kernel_timing are set (they read back on the host).
+ * Errors: SEL_EINVAL (NULL pointer, n < 0, debug/kernel_timing set), SEL_ENOMEM,
+ * SEL_ECUDA; per-field errors land in out[i].status. */
+int sel_estimate_batch_async(sel_plan_t plan, const float *const *d_fields, int n, void *stream,
+                             sel_result *out);
+
 /* End-to-end entry: fields in HOST memory (pinned for full speed).  The plan
  * stages each field into device buffers with cudaMemcpyAsync on an internal
  * copy stream, double-buffered so the copy of field i+1 overlaps the estimate

@@ -24,7 +24,7 @@ EB_ABS, EB_REL = 0, 1
 
 # every entry point declared in include/sel.h
 EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_batch",
-           "sel_estimate_batch_host", "sel_choose", "sel_debug_copy", "sel_kernel_times",
+           "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_debug_copy", "sel_kernel_times",
            "sel_processed_blocks", "sel_processed_values", "sel_workspace_bytes",
            "sel_launch_count", "sel_plan_destroy", "sel_strerror")
 
@@ -74,6 +74,8 @@ def lib():
         L.sel_estimate.restype = C.c_int
         L.sel_estimate_batch.argtypes = [P, P, C.c_int, P, P]
         L.sel_estimate_batch.restype = C.c_int
+        L.sel_estimate_batch_async.argtypes = [P, P, C.c_int, P, P]
+        L.sel_estimate_batch_async.restype = C.c_int
         L.sel_estimate_batch_host.argtypes = [P, P, C.c_int, P, P]
         L.sel_estimate_batch_host.restype = C.c_int
         L.sel_choose.argtypes = [C.POINTER(Result), C.POINTER(C.c_int32)]
@@ -192,6 +194,33 @@ class Plan:
         out = (Result * n)()
         _check(lib().sel_estimate_batch(self._h, ptrs, n, _stream_ptr(stream), out))
         return [o.to_dict() for o in out]
+
+    def estimate_batch_async(self, fields, out, stream=None):
+        """Enqueue the estimate of `fields` and the copy of their results into `out`
+        (a pinned-host or CUDA uint8 tensor from `results_buffer`) on `stream`; returns
+        at once.  Decode with `decode_results(out)` after synchronising the stream."""
+        n = len(fields)
+        if out.numel() < n * C.sizeof(Result):
+            raise ValueError("results buffer too small")
+        ptrs = (C.c_void_p * n)(*[_device_ptr(f) for f in fields])
+        _check(lib().sel_estimate_batch_async(self._h, ptrs, n, _stream_ptr(stream),
+                                              C.c_void_p(out.data_ptr())))
+
+    @staticmethod
+    def results_buffer(n: int, device="pinned"):
+        """uint8 tensor for n results: page-locked host memory, or a CUDA device."""
+        import torch
+        nb = n * C.sizeof(Result)
+        if device == "pinned":
+            return torch.empty(nb, dtype=torch.uint8).pin_memory()
+        return torch.empty(nb, dtype=torch.uint8, device=device)
+
+    @staticmethod
+    def decode_results(buf, n: int | None = None) -> list[dict]:
+        raw = bytes(buf.cpu().numpy().tobytes()) if buf.is_cuda else bytes(buf.numpy().tobytes())
+        n = len(raw) // C.sizeof(Result) if n is None else n
+        arr = (Result * n).from_buffer_copy(raw[: n * C.sizeof(Result)])
+        return [o.to_dict() for o in arr]
 
     def estimate_batch_host(self, fields, stream=None) -> list[dict]:
         n = len(fields)

@@ -43,7 +43,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not (force or stale()):
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", tmp, *SOURCES]
+    extra = os.environ.get("SEL_EXTRA_NVCC_FLAGS", "").split()   # developer builds only
+    cmd = [NVCC, *FLAGS, *extra, *(["-Xptxas", "-v"] if verbose else []), "-o", tmp, *SOURCES]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

@@ -542,6 +542,26 @@ int sel_estimate_batch(sel_plan_t p, const float *const *d_fields, int n, void *
   return finish(p, st, n, out);
 }
 
+int sel_estimate_batch_async(sel_plan_t p, const float *const *d_fields, int n, void *stream,
+                             sel_result *out) {
+  if (!p || !d_fields || !out || n < 0 || p->timing || p->debug) return SEL_EINVAL;
+  if (n == 0) return SEL_OK;
+  for (int f = 0; f < n; ++f) if (!d_fields[f]) return SEL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_results(p, n);
+  if (rc) return rc;
+  if (batch_ok(p, d_fields, n)) {
+    if ((rc = enqueue_batch(p, d_fields, n, st))) return rc;
+  } else if (n >= 2 && p->pipeline) {
+    if ((rc = enqueue_pipelined(p, d_fields, n, st))) return rc;
+  } else {
+    for (int f = 0; f < n; ++f)
+      if ((rc = enqueue_field(p, d_fields[f], st, f))) return rc;
+  }
+  CK(cudaMemcpyAsync(out, p->d_res, sizeof(sel_result) * (size_t)n, cudaMemcpyDefault, st));
+  return SEL_OK;
+}
+
 int sel_estimate_batch_host(sel_plan_t p, const float *const *h_fields, int n, void *stream,
                             sel_result *out) {
   if (!p || !h_fields || !out || n < 0) return SEL_EINVAL;

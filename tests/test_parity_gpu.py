@@ -245,6 +245,31 @@ def test_batch_kernel_tiny_stacks(sel, orc, nf, shape):
         compare_scalars(out[i], orc.estimate(x, 1e-3), f"tiny{nf}/{i}")
 
 
+@pytest.mark.parametrize("where", ["pinned", "cuda"])
+@pytest.mark.parametrize("batch_kernel", [1, 0])
+def test_estimate_batch_async(sel, orc, where, batch_kernel):
+    """Stream-ordered entry: several calls enqueued back to back on one stream, each
+    into its own results buffer, read after one synchronise -- equal to the oracle."""
+    shape = (72, 100)
+    rng = np.random.default_rng(7)
+    stacks = [[np.cumsum(rng.standard_normal(shape), axis=k % 2).astype(np.float32) * (k + 1)
+               for k in range(3)] for _ in range(3)]
+    dev = [[torch.from_numpy(x).cuda() for x in st] for st in stacks]
+    with sel.Plan(shape, 1e-3) as p:
+        p.set_option("batch_kernel", batch_kernel)
+        bufs = [p.results_buffer(3, "pinned" if where == "pinned" else "cuda") for _ in stacks]
+        for d, b in zip(dev, bufs):
+            p.estimate_batch_async(d, b)
+        torch.cuda.synchronize()
+        for st, b in zip(stacks, bufs):
+            out = p.decode_results(b, 3)
+            for i, x in enumerate(st):
+                compare_scalars(out[i], orc.estimate(x, 1e-3), f"async/{i}")
+        p.set_option("kernel_timing", 1)
+        with pytest.raises(sel.SelError):
+            p.estimate_batch_async(dev[0], bufs[0])
+
+
 @pytest.mark.parametrize("shape", [(96, 128), (20, 24, 36), (1, 1, 8)])
 def test_batch_kernel_many_fields(sel, orc, shape):
     """k_batch over a longer stack (parity buffers reused, phases overlap) == oracle."""
