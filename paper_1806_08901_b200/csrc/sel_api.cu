@@ -54,6 +54,7 @@ struct sel_plan_st {
   TileLaunch tl[2] = {};                          // [debug]
   BatchSizes bs{};                                // persistent batch kernel sizes
   int use_batch = 1;
+  int groups = 0;                 // k_batch CTA groups (0: auto, batch_groups)
   void *bstate = nullptr;                         // batch kernel state (grows with n)
   cudaEvent_t bev[2] = {nullptr, nullptr};        // kernel_timing around k_batch
   bool batch_timed = false;
@@ -204,8 +205,25 @@ bool batch_ok(sel_plan_t p, const float *const *x, int n) {
   return true;
 }
 
+// CTA groups for k_batch: G groups each run every G-th field on sm_count / G CTAs, so a
+// CTA flushes its histogram G x less often; the fields whose range pass is ahead of
+// their tiles (kLagT per group) must stay in L2 (~126 MB), hence the byte budget.
+int batch_groups(sel_plan_t p, int n) {
+  int G = p->groups;
+  if (G <= 0) {                   // measured: ~80 MB of fields in flight
+    const double fb = (double)p->geo.N * 4.0;
+    G = (int)(80e6 / fb);
+    if (G > 32) G = 32;
+    if (G > n / 2) G = n / 2;     // keep >= 2 fields per group (tail balance)
+  }
+  if (G > n) G = n;
+  if (G > p->sm_count) G = p->sm_count;
+  return G < 1 ? 1 : G;
+}
+
 int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
-  const size_t need = batch_state_bytes(n, p->bs, p->tl[0].tg.ntasks);
+  const int G = batch_groups(p, n);
+  const size_t need = batch_state_bytes(n, p->bs, p->tl[0].tg.ntasks, G);
   if (need > p->bstate_cap) {
     if (p->bstate) {
       CK(cudaStreamSynchronize(st));
@@ -233,7 +251,7 @@ int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
     }
   }
   int rc = launch_batch(g, p->tl[0], p->bs, x, n, p->bstate, p->bstate_cap, fa, p->mode, p->eb,
-                        p->d_res, p->sm_count, st, p->timing ? p->bev : nullptr);
+                        p->d_res, p->sm_count, G, st, p->timing ? p->bev : nullptr);
   if (rc) return cuda_fail(cudaGetLastError(), "k_batch launch");
   p->launches += 1;
   p->batch_timed = p->timing;
@@ -487,6 +505,11 @@ int sel_set_option(sel_plan_t p, const char *key, double value) {
   if (!strcmp(key, "debug")) {
     p->debug = value != 0.0;
     if (p->debug) return ensure_debug(p);
+    return SEL_OK;
+  }
+  if (!strcmp(key, "groups")) {
+    if (!(value >= 0.0 && value <= 148.0)) return SEL_EINVAL;
+    p->groups = (int)value;
     return SEL_OK;
   }
   if (!strcmp(key, "batch_kernel")) {

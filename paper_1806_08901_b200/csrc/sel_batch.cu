@@ -58,7 +58,6 @@ struct BatchArgs {
   int64_t N;
   int nR, nT, phase;              // tasks per field (F: kFinTasks); phase = kFinTasks + nR + nT
   int rchunk;                     // floats per R task
-  long long ntotal;               // (nf + 2) * phase
   FinalizeArgs fa;
   int mode;
   double eb;
@@ -70,10 +69,11 @@ struct BatchArgs {
   unsigned int *tdone;            // [nf] tile tasks whose histogram counts are flushed
   unsigned int *fdone;            // [nf]
   unsigned int *fin_ready;        // [nf]
-  unsigned long long *hist[kRing]; // per field f % kRing
-  Partial *tpart[kRing];          // [nT * CW]
-  FPart *fpart[kRing];            // [kFinTasks]
-  unsigned int *task_ctr;         // [1]
+  int G;                          // CTA groups: group g = blockIdx % G runs fields f = g (mod G)
+  unsigned long long *hist;       // [G * kRing][kNSlots], slot ring(f)
+  Partial *tpart;                 // [G * kRing][nT * CW]
+  FPart *fpart;                   // [G * kRing][kFinTasks]
+  unsigned int *task_ctr;         // [G]
   sel_result *results;            // [nf]
   unsigned long long *prof;       // optional [gridDim * 8] cycle counters (warp 0 of each CTA)
 };
@@ -84,26 +84,33 @@ enum { KIND_NONE = 0, KIND_R = 1, KIND_T = 2, KIND_F = 3 };
 // R(p) [nR] and T(p-kLagT) [nT] interleaved (Bresenham); absent fields contribute nothing.
 // R runs kLagT phases ahead of its tiles (its results are published at the next phase
 // boundary), F runs two phases after them (every CTA has flushed by then).
-__device__ __forceinline__ bool in_range(const BatchArgs &a, int f) { return f >= 0 && f < a.nf; }
+// With G CTA groups every group runs this sequence over its own fields (local index
+// l <-> field l * G + g) with its own task counter, so a CTA meets G x fewer fields.
+__device__ __forceinline__ bool in_range(int nfl, int f) { return f >= 0 && f < nfl; }
 
-__device__ __forceinline__ long long phase_size(const BatchArgs &a, int p) {
-  return (long long)(in_range(a, p - kLagF) ? kFinTasks : 0) + (in_range(a, p) ? a.nR : 0) +
-         (in_range(a, p - kLagT) ? a.nT : 0);
+__device__ __forceinline__ long long phase_size(const BatchArgs &a, int nfl, int p) {
+  return (long long)(in_range(nfl, p - kLagF) ? kFinTasks : 0) + (in_range(nfl, p) ? a.nR : 0) +
+         (in_range(nfl, p - kLagT) ? a.nT : 0);
 }
 
-__device__ __forceinline__ void decode(const BatchArgs &a, long long tau, int &kind, int &f, int &id,
-                                       int &phase) {
-  // phases 0 .. kLagF-1 are the ramp, kLagF .. nf-1 share one size, then the tail
+// buffer slot of field f: kRing per group, reused by field f + kRing * G
+__device__ __forceinline__ int ring(const BatchArgs &a, int f) {
+  return (f % a.G) * kRing + (f / a.G) % kRing;
+}
+
+__device__ __forceinline__ void decode(const BatchArgs &a, int nfl, long long tau, int &kind, int &f,
+                                       int &id, int &phase) {
+  // phases 0 .. kLagF-1 are the ramp, kLagF .. nfl-1 share one size, then the tail
   int p = 0;
   long long m = tau;
-  const int ramp_end = a.nf < kLagF ? a.nf : kLagF;
+  const int ramp_end = nfl < kLagF ? nfl : kLagF;
   for (; p < ramp_end; ++p) {
-    const long long sz = phase_size(a, p);
+    const long long sz = phase_size(a, nfl, p);
     if (m < sz) break;
     m -= sz;
   }
   if (p == ramp_end) {
-    const int nmid = a.nf > kLagF ? a.nf - kLagF : 0;
+    const int nmid = nfl > kLagF ? nfl - kLagF : 0;
     const long long S = (long long)kFinTasks + a.nR + a.nT;
     if (nmid > 0 && m < nmid * S) {
       const int q = (int)(m / S);
@@ -112,17 +119,17 @@ __device__ __forceinline__ void decode(const BatchArgs &a, long long tau, int &k
     } else {
       m -= (long long)nmid * S;
       p = ramp_end + nmid;
-      while (m >= phase_size(a, p)) { m -= phase_size(a, p); ++p; }
+      while (m >= phase_size(a, nfl, p)) { m -= phase_size(a, nfl, p); ++p; }
     }
   }
   phase = p;
-  const int nF = in_range(a, p - kLagF) ? kFinTasks : 0;
+  const int nF = in_range(nfl, p - kLagF) ? kFinTasks : 0;
   if (m < nF) {
     kind = KIND_F; f = p - kLagF; id = (int)m;
     return;
   }
   m -= nF;
-  const long long nRp = in_range(a, p) ? a.nR : 0, nTp = in_range(a, p - kLagT) ? a.nT : 0;
+  const long long nRp = in_range(nfl, p) ? a.nR : 0, nTp = in_range(nfl, p - kLagT) ? a.nT : 0;
   const long long M = nRp + nTp;
   const long long r0 = m * nRp / M, r1 = (m + 1) * nRp / M;
   if (r1 > r0) { kind = KIND_R; f = p; id = (int)r0; }
@@ -192,6 +199,9 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int grp = (int)(blockIdx.x % (unsigned)a.G);
+  const int nfl = (a.nf - grp + a.G - 1) / a.G;                  // this group's fields
+  const long long ntot = (long long)nfl * (a.nR + a.nT + kFinTasks);
   if (tid == 0) {
     s_tbl_used = 0;
     for (int k = 0; k < 2; ++k) {
@@ -218,14 +228,17 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_last));
       // the next task id is fetched one task ahead, so the atomic's round trip overlaps
       // the wait for a free stage
-      long long next = (long long)atomicAdd(a.task_ctr, 1u);
+      long long next = (long long)atomicAdd(a.task_ctr + grp, 1u);
       for (;;) {
         const long long tau = next;
-        if (tau < a.ntotal) next = (long long)atomicAdd(a.task_ctr, 1u);
+        if (tau < ntot) next = (long long)atomicAdd(a.task_ctr + grp, 1u);
         mbar_wait(&empty_bar[stage], ph ^ 1u);
         int kind = KIND_NONE, f = 0, id = 0, phase = 0;
-        if (tau < a.ntotal) decode(a, tau, kind, f, id, phase);
-        stage_desc[stage] = make_int4(tau >= a.ntotal ? -1 : kind, f, id, phase);
+        if (tau < ntot) {
+          decode(a, nfl, tau, kind, f, id, phase);
+          f = f * a.G + grp;                 // global field index
+        }
+        stage_desc[stage] = make_int4(tau >= ntot ? -1 : kind, f, id, phase);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
         if (kind == KIND_T) {
           const int btk = id % a.tg.ntk;
@@ -249,7 +262,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
           mbar_arrive(&full_bar[stage]);   // F / padding / sentinel: no data
         }
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
-        if (tau >= a.ntotal) break;
+        if (tau >= ntot) break;
       }
     }
     return;
@@ -302,7 +315,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   };
 
   auto flush = [&]() {             // all consumers, same task: move smem histogram to global
-    unsigned long long *gh = a.hist[cur % kRing];
+    unsigned long long *gh = a.hist + (size_t)ring(a, cur) * kNSlots;
     const long long q0 = PCLOCK();
     ovf_flush(ovf, gh);
     ovf = 0;
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       const int pp = cur_phase & 1;
       const unsigned int cnt = s_rcnt[pp];
       if (cnt) {
-        const int g = cur_phase;                                  // R(p) belongs to field p
+        const int g = cur_phase * a.G + grp;                      // R(p) belongs to local field p
         if (s_rmin[pp] != 0xffffffffu) atomicMin(a.rmin + g, s_rmin[pp]);
         if (s_rmax[pp] != 0u) atomicMax(a.rmax + g, s_rmax[pp]);
         if (s_rbad[pp]) atomicOr(a.rbad + g, 1u);
@@ -370,7 +383,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
     // fin_ready, finalize waits on tdone) and at the end; range tasks never block
     const bool may_block = end || kind == KIND_F || (kind == KIND_T && f != cur);
     release();                     // last boundary's flush / publish (their atomics drained)
-    while (cur_phase < (end ? a.nf + kLagF + 1 : phase)) {       // phase change(s)
+    while (cur_phase < (end ? nfl + kLagF + 1 : phase)) {        // phase change(s)
       leave_phase();
       ++cur_phase;
       release();                   // several phase changes in a row (empty phases, the end)
@@ -386,7 +399,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       if (cur < 0) {               // first tile of field f here: params, parity buffer free
         if (tid == 0) {
           spin_until(a.params_ready + f, 1u);
-          if (f >= kRing) spin_until(a.fin_ready + f - kRing, 1u);
+          if (f >= kRing * a.G) spin_until(a.fin_ready + f - kRing * a.G, 1u);   // slot's last user
           s_prm = a.params[f];
         }
         consumer_sync<NC>();
@@ -400,11 +413,12 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       double terr = 0.0;
       const int4 tc = stage_tile[stage];
       tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hlane, htrash,
-                             tbl, &s_tbl_used, a.hist[f % kRing], ovf, nodbg, tbits, terr);
+                             tbl, &s_tbl_used, a.hist + (size_t)ring(a, f) * kNSlots, ovf, nodbg,
+                             tbits, terr);
       ++cur_tasks;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
-      task_store(a.tpart[f % kRing], id * CW + warp, tbits, terr);
+      task_store(a.tpart + (size_t)ring(a, f) * a.nT * CW, id * CW + warp, tbits, terr);
     } else if (kind == KIND_R) {
       // ---- min / max / non-finite of the staged chunk (R1) by kRWarps consumer warps
       // (rotating with the task id); the others release the stage at once and move on.
@@ -448,7 +462,9 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
       if (tid == 0) spin_until(a.tdone + f, (unsigned)a.nT);
       consumer_sync<NC>();
-      unsigned long long *gh = a.hist[f % kRing];
+      unsigned long long *gh = a.hist + (size_t)ring(a, f) * kNSlots;
+      const Partial *tpf = a.tpart + (size_t)ring(a, f) * a.nT * CW;
+      FPart *fpf = a.fpart + (size_t)ring(a, f) * kFinTasks;
       // ---- 1/8 of the histogram: sum c log2(N/c), re-zero; and 1/8 of the tile partials
       const double Nsz = (double)a.fa.n_sz;
       const double lN = log2(Nsz);
@@ -470,8 +486,8 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       double err = 0.0;
       unsigned long long bits = 0;
       for (int t = p0 + tid; t < p1; t += NC) {
-        bits += __ldcg(&a.tpart[f % kRing][t].bits);
-        err += __ldcg(&a.tpart[f % kRing][t].err);
+        bits += __ldcg(&tpf[t].bits);
+        err += __ldcg(&tpf[t].err);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -487,17 +503,17 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
         for (int w = 1; w < CW; ++w) { acc += s_red[0][w]; err += s_red[1][w]; bits += s_redu[0][w]; novf += s_redu[1][w]; }
         FPart fp;
         fp.acc = acc; fp.err = err; fp.bits = bits; fp.ovf = novf;
-        a.fpart[f % kRing][id] = fp;
+        fpf[id] = fp;
         fence_acq_rel_gpu();
         if (atomicAdd(a.fdone + f, 1u) == (unsigned)kFinTasks - 1) {   // last: result f
           fence_acq_rel_gpu();
           double S = 0.0, errs = 0.0;
           unsigned long long tb = 0, ov = 0;
           for (int k = 0; k < kFinTasks; ++k) {
-            S += __ldcg(&a.fpart[f % kRing][k].acc);
-            errs += __ldcg(&a.fpart[f % kRing][k].err);
-            tb += __ldcg(&a.fpart[f % kRing][k].bits);
-            ov += __ldcg(&a.fpart[f % kRing][k].ovf);
+            S += __ldcg(&fpf[k].acc);
+            errs += __ldcg(&fpf[k].err);
+            tb += __ldcg(&fpf[k].bits);
+            ov += __ldcg(&fpf[k].ovf);
           }
           const Params prm = a.params[f];
           const double mse = errs / (double)a.fa.n_values;
@@ -547,15 +563,17 @@ int batch_sizes(const Geo &g, BatchSizes *bs) {
   return SEL_OK;
 }
 
-size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT) {
-  return (size_t)nf * (sizeof(Params) + 8 * 4 + sizeof(CUtensorMap) + 8) +
-         kRing * ((size_t)kNSlots * 8 + (size_t)nT * bs.cw * sizeof(Partial) + kFinTasks * sizeof(FPart) + 768) +
-         4096;
+size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G) {
+  return (size_t)nf * (sizeof(Params) + 8 * 4 + sizeof(CUtensorMap) + 8) + 64 +
+         (size_t)G * kRing * ((size_t)kNSlots * 8 + (size_t)nT * bs.cw * sizeof(Partial) +
+                              kFinTasks * sizeof(FPart)) +
+         8192;
 }
 
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
-                 sel_result *d_results, int sm_count, cudaStream_t st, cudaEvent_t *ev) {
+                 sel_result *d_results, int sm_count, int G, cudaStream_t st, cudaEvent_t *ev) {
+  if (G < 1 || G > nf || G > sm_count) return SEL_EINVAL;
   // state layout (device): tmaps | xs | params | counters | hist x2 | tpart x2 | fpart x2
   char *b = (char *)state;
   size_t off = 0;
@@ -569,15 +587,12 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   CUtensorMap *tmaps = (CUtensorMap *)take(sizeof(CUtensorMap) * nf, 128);
   const float **xs = (const float **)take(sizeof(float *) * nf);
   Params *params = (Params *)take(sizeof(Params) * nf);
-  unsigned int *ctrs = (unsigned int *)take(sizeof(unsigned int) * (8 * (size_t)nf + 1));
-  unsigned long long *hst[kRing];
-  Partial *tp[kRing];
-  FPart *fp[kRing];
-  for (int k = 0; k < kRing; ++k) {
-    hst[k] = (unsigned long long *)take((size_t)kNSlots * 8);
-    tp[k] = (Partial *)take(sizeof(Partial) * (size_t)nT * bs.cw);
-    fp[k] = (FPart *)take(sizeof(FPart) * kFinTasks);
-  }
+  const size_t nctr = 8 * (size_t)nf + (size_t)G;
+  unsigned int *ctrs = (unsigned int *)take(sizeof(unsigned int) * nctr);
+  const size_t nslot = (size_t)G * kRing;
+  unsigned long long *hst = (unsigned long long *)take((size_t)kNSlots * 8 * nslot);
+  Partial *tp = (Partial *)take(sizeof(Partial) * (size_t)nT * bs.cw * nslot);
+  FPart *fp = (FPart *)take(sizeof(FPart) * kFinTasks * nslot);
   if (off > state_bytes) return SEL_EINVAL;
   // host-built tensor maps and pointer table, one H2D copy each (staged in pinned memory
   // by the caller? small: a few KB -> plain cudaMemcpyAsync from pageable is fine)
@@ -588,11 +603,9 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   if (cudaMemcpyAsync(tmaps, h_maps.data(), sizeof(CUtensorMap) * nf, cudaMemcpyHostToDevice, st) !=
           cudaSuccess ||
       cudaMemcpyAsync(xs, d_fields, sizeof(float *) * nf, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-      cudaMemsetAsync(ctrs, 0, sizeof(unsigned int) * (8 * (size_t)nf + 1), st) != cudaSuccess ||
+      cudaMemsetAsync(ctrs, 0, sizeof(unsigned int) * nctr, st) != cudaSuccess ||
       cudaMemsetAsync(ctrs + 6 * (size_t)nf, 0xff, sizeof(unsigned int) * nf, st) != cudaSuccess ||
-      cudaMemsetAsync(hst[0], 0, (size_t)kNSlots * 8, st) != cudaSuccess ||
-      cudaMemsetAsync(hst[1], 0, (size_t)kNSlots * 8, st) != cudaSuccess ||
-      cudaMemsetAsync(hst[2], 0, (size_t)kNSlots * 8, st) != cudaSuccess)
+      cudaMemsetAsync(hst, 0, (size_t)kNSlots * 8 * nslot, st) != cudaSuccess)
     return SEL_ECUDA;
   BatchArgs a;
   a.tmaps = tmaps;
@@ -604,7 +617,6 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   a.nT = nT;
   a.phase = kFinTasks + bs.nR + nT;
   a.rchunk = bs.rchunk;
-  a.ntotal = (long long)nf * (bs.nR + nT + kFinTasks);    // every real task exactly once
   a.fa = fa;
   a.mode = mode;
   a.eb = eb;
@@ -618,11 +630,10 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   a.rmin = ctrs + 6 * nf;
   a.rbad = ctrs + 7 * nf;
   a.task_ctr = ctrs + 8 * nf;
-  for (int k = 0; k < kRing; ++k) {
-    a.hist[k] = hst[k];
-    a.tpart[k] = tp[k];
-    a.fpart[k] = fp[k];
-  }
+  a.G = G;
+  a.hist = hst;
+  a.tpart = tp;
+  a.fpart = fp;
   a.results = d_results;
   a.prof = g_batch_prof;
   const void *fn = g.ndims == 3 ? batch_fn<3>() : batch_fn<2>();

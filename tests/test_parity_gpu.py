@@ -245,6 +245,20 @@ def test_batch_kernel_tiny_stacks(sel, orc, nf, shape):
         compare_scalars(out[i], orc.estimate(x, 1e-3), f"tiny{nf}/{i}")
 
 
+@pytest.mark.parametrize("groups", [1, 2, 3, 5])
+def test_batch_groups(sel, orc, groups):
+    """CTA groups (each group runs every G-th field) give the oracle's results."""
+    shape = (40, 300)
+    rng = np.random.default_rng(groups)
+    xs = [np.cumsum(rng.standard_normal(shape), axis=1).astype(np.float32) for _ in range(7)]
+    ts = [torch.from_numpy(x).cuda() for x in xs]
+    with sel.Plan(shape, 1e-3) as p:
+        p.set_option("groups", groups)
+        out = p.estimate_batch(ts)
+    for i, x in enumerate(xs):
+        compare_scalars(out[i], orc.estimate(x, 1e-3), f"G{groups}/{i}")
+
+
 @pytest.mark.parametrize("where", ["pinned", "cuda"])
 @pytest.mark.parametrize("batch_kernel", [1, 0])
 def test_estimate_batch_async(sel, orc, where, batch_kernel):
