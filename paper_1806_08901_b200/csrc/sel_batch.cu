@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       for (;;) {
         const long long tau = next;
         if (tau < ntot) next = (long long)atomicAdd(a.task_ctr + grp, 1u);
-        mbar_wait(&empty_bar[stage], ph ^ 1u);
+        mbar_wait_sleep(&empty_bar[stage], ph ^ 1u);
         int kind = KIND_NONE, f = 0, id = 0, phase = 0;
         if (tau < ntot) {
           decode(a, nfl, tau, kind, f, id, phase);

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
       for (;;) {
         const int t = next;
         if (t < tg.ntasks) next = (int)atomicAdd(ws.task_ctr, 1u);
-        mbar_wait(&empty_bar[stage], ph ^ 1u);
+        mbar_wait_sleep(&empty_bar[stage], ph ^ 1u);
         if (t >= tg.ntasks) {           // sentinel stage: consumers stop here
           stage_task[stage] = make_int4(t, 0, 0, 0);
           mbar_arrive(&full_bar[stage]);
@@ -136,7 +136,7 @@ const void *tile_fn(bool dbg) {
 
 bool tile_supported(const Geo &g) {
   return (g.ndims == 2 || g.ndims == 3) && g.s[0] == 1 && g.s[1] == 1 && g.s[2] == 1 &&
-         g.n[2] % 4 == 0 && g.n[2] < (1LL << 31) && g.n[1] < (1LL << 31) && g.n[0] < (1LL << 31);
+         g.n[2] % 4 == 0 && g.n[2] < (1LL << 30) && g.n[1] < (1LL << 30) && g.n[0] < (1LL << 30);
 }
 
 int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl) {

@@ -27,10 +27,11 @@ struct TileCfg {
   static constexpr int STAGES = D == 3 ? 2 : 4;
   static constexpr int COPIES = D == 3 ? 4 : 8;                   // histogram lane copies
   static constexpr int HIST_WORDS = (COPIES + 1) * kHStride;   // + trash copy
-  // second level: one packed 16-bit-counter table of TB slots centred on code 0 for the
-  // codes outside the lane-copy window (wide distributions: noise, coarse data)
-  static constexpr int TB = D == 3 ? 17408 : 27392;   // leaves ~2.5 KB of the SM for k_minmax + k_finalize
-  static constexpr int TBL_WORDS = TB / 2;
+  // second level: one table of TB 32-bit counters centred on code 0 for the codes
+  // outside the lane-copy window (wide distributions: noise, fronts, coarse data)
+  static constexpr int TB = D == 3 ? 8704 : 13696;    // leaves ~2.5 KB of the SM for k_minmax + k_finalize
+  static constexpr int TBL_WORDS = TB;
+  static constexpr uint32_t kTOff = kSlotOff + (uint32_t)(kCenter - TB / 2);   // bits -> table slot
   static constexpr size_t SMEM = 128 + (size_t)STAGES * STAGE_FLOATS * 4 + HIST_WORDS * 4 +
                                  TBL_WORDS * 4 + STAGES * 48 + 16;
 };
@@ -51,6 +52,24 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// non-blocking probe of a phase (producers poll it with a sleep: a suspended try_wait
+// wakes on every barrier event of the CTA and would steal issue slots from consumers)
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) __nanosleep(64);
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
@@ -130,14 +149,16 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
   constexpr int CW = Cfg::CW;
   constexpr int SZ = Tab<D>::SIZE;
   constexpr int NPL = D == 3 ? 4 : 1;
-  const int64_t n0 = tg.n[0], n1 = tg.n[1], n2 = tg.n[2];
+  // per-axis extents and block coordinates fit 32 bits (tile_supported); only the debug
+  // dumps form 64-bit linear indices
+  const int n0 = (int)tg.n[0], n1 = (int)tg.n[1], n2 = (int)tg.n[2];
     const int bj = btj * CW + warp;
-    const int64_t bk = (int64_t)btk * 32 + lane;
+    const int bk = btk * 32 + lane;
     tbits = 0;
     terr = 0.0;
     if (ok && bj < tg.nb[1]) {
       const bool activeK = bk < tg.nb[2];
-      const int64_t I0 = 4 * (int64_t)bi, J0 = 4 * (int64_t)bj, K0 = 4 * bk;
+      const int I0 = 4 * bi, J0 = 4 * bj, K0 = 4 * bk;
       const float *wrow = S + (4 * warp) * kBoxK;   // smem row of j = J0 - 1 (plane 0)
       unsigned int *const hcopy = activeK ? hlane : htrash;
       // ---------------- SZ: nested differences on the tile (R4), codes -> histogram (R5)
@@ -161,15 +182,23 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
           }
       }
 #pragma unroll 1
+      float blk2[D == 2 ? 16 : 1];   // 2D: the ZFP block is rows 1..4 of the SZ plane
       for (int p = 0; p < NPL; ++p) {
-        const int64_t i = I0 + p;
+        const int i = I0 + p;
         float v[5][4], h[5], d1up[4];
         load_plane(wrow + (D == 3 ? (p + 1) * Cfg::PLANE : 0), lane, v, h);
+        if constexpr (D == 2) {       // rows past the field's edge replicate the last (R17)
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              blk2[4 * r + c] = (r == 0 || J0 + r < n1) ? v[r + 1][c] : blk2[4 * (r - 1) + c];
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) d1up[c] = v[0][c] - (c ? v[0][c - 1] : h[0]);
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int64_t j = J0 + r;
+          const int j = J0 + r;
           if (i >= n0 || j >= n1) break;              // padded rows/planes: no SZ point
           uint32_t w[4];
           uint32_t any = 0;
@@ -200,33 +229,30 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
               for (int c = 0; c < 4; ++c) {
                 if (orow && lane == 0 && c == 0) continue;
                 const uint32_t sl = w[c] + (kHOff - kSlotOff);
-                dbg.codes[(i * n1 + j) * n2 + K0 + c] = sl > 65534u ? kOvfSlot : (int32_t)sl;
+                dbg.codes[((int64_t)i * n1 + j) * n2 + K0 + c] = sl > 65534u ? kOvfSlot : (int32_t)sl;
               }
             }
           }
-          // out-of-window codes: one warp-uniform branch per row
+          // out-of-window codes (wide distributions): one warp-uniform branch per row; the
+          // table takes them with one predicated atomic each, the rest (rare) go to the
+          // global histogram or the overflow count
           if (__any_sync(0xffffffffu, activeK && any >= (uint32_t)kHBins)) {
-            if (activeK) {
+            uint32_t far = 0u;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t tb = w[c] + (kHOff - Cfg::kTOff);
+              const bool out = activeK && w[c] >= (uint32_t)kHBins;
+              if (out && tb < (uint32_t)Cfg::TB) atomicAdd(tbl + tb, 1u);
+              far |= (out && tb >= (uint32_t)Cfg::TB) ? (1u << c) : 0u;
+            }
+            if (lane == 0) *tbl_used = 1;
+            if (__any_sync(0xffffffffu, far != 0u)) {
 #pragma unroll
               for (int c = 0; c < 4; ++c)
-                if (w[c] >= (uint32_t)kHBins) {
+                if (far & (1u << c)) {
                   const uint32_t sl = w[c] + (kHOff - kSlotOff);
-                  const uint32_t tb = sl - (uint32_t)(kCenter - Cfg::TB / 2);
-                  if (sl > 65534u) {
-                    ++ovf;
-                  } else if (tb < (uint32_t)Cfg::TB) {
-                    *tbl_used = 1;
-                    // packed 16-bit counter; the increment that takes it to 0x8000 moves
-                    // 0x8000 counts to the global histogram, so it never carries
-                    const uint32_t sh = (tb & 1u) << 4;
-                    const uint32_t old = atomicAdd(tbl + (tb >> 1), 1u << sh);
-                    if (((old >> sh) & 0xffffu) == 0x7fffu) {
-                      atomicSub(tbl + (tb >> 1), 0x8000u << sh);
-                      atomicAdd(ghist + sl, 0x8000ull);
-                    }
-                  } else {
-                    atomicAdd(ghist + sl, 1ull);
-                  }
+                  if (sl > 65534u) ++ovf;
+                  else atomicAdd(ghist + sl, 1ull);
                 }
             }
           }
@@ -235,17 +261,22 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
       // ---------------- ZFP on the lane's block, edge-replicated at the far edges (R17)
       if (activeK) {
         float blk[SZ];
+        if constexpr (D == 2) {
 #pragma unroll
-        for (int p = 0; p < NPL; ++p) {
-          const int64_t ic = min(I0 + p, n0 - 1) - I0;          // 0..3 (3D)
-          const float *pbase = S + (D == 3 ? (ic + 1) * Cfg::PLANE : 0);
+          for (int n = 0; n < 16; ++n) blk[n] = blk2[n];
+        } else {
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int64_t jc = min(J0 + r, n1 - 1) - J0;         // 0..3
-            const float4 q = *reinterpret_cast<const float4 *>(
-                pbase + (4 * warp + 1 + jc) * kBoxK + 4 + 4 * lane);
-            const int o = (p * 4 + r) * 4;
-            blk[o] = q.x; blk[o + 1] = q.y; blk[o + 2] = q.z; blk[o + 3] = q.w;
+          for (int p = 0; p < NPL; ++p) {
+            const int ic = min(I0 + p, n0 - 1) - I0;          // 0..3, edge-replicated
+            const float *pbase = S + (ic + 1) * Cfg::PLANE;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int jc = min(J0 + r, n1 - 1) - J0;         // 0..3
+              const float4 q = *reinterpret_cast<const float4 *>(
+                  pbase + (4 * warp + 1 + jc) * kBoxK + 4 + 4 * lane);
+              const int o = (p * 4 + r) * 4;
+              blk[o] = q.x; blk[o + 1] = q.y; blk[o + 2] = q.z; blk[o + 3] = q.w;
+            }
           }
         }
         uint32_t bits;
@@ -257,7 +288,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
         tbits = bits;
         terr = E;
         if constexpr (DBG) {
-          const int64_t tb = (D == 3 ? ((int64_t)bi * tg.nb[1] + bj) : (int64_t)bj) * tg.nb[2] + bk;
+          const int64_t tb = (D == 3 ? ((int64_t)bi * tg.nb[1] + bj) : (int64_t)bj) * tg.nb[2] + bk;   // block index
           dbg.emax[tb] = emax; dbg.bits[tb] = bits; dbg.err[tb] = E;
 #pragma unroll
           for (int n = 0; n < SZ; ++n) { dbg.coef[tb * SZ + n] = cf[n]; dbg.uword[tb * SZ + n] = u[n]; }
@@ -283,12 +314,12 @@ __device__ __forceinline__ void tile_hist_flush(unsigned int *hist, unsigned int
     if (c) atomicAdd(ghist + (kCenter - kHBins / 2) + i, c);
   }
   if (!*tbl_used) return;               // no code outside the lane-copy window: table is zero
-  for (int i = tid; i < Cfg::TBL_WORDS; i += nthr) {
+  for (int i = tid; i < Cfg::TB; i += nthr) {
     const uint32_t v = tbl[i];
-    tbl[i] = 0u;
-    unsigned long long *g = ghist + (kCenter - Cfg::TB / 2) + 2 * i;
-    if (v & 0xffffu) atomicAdd(g, (unsigned long long)(v & 0xffffu));
-    if (v >> 16) atomicAdd(g + 1, (unsigned long long)(v >> 16));
+    if (v) {
+      tbl[i] = 0u;
+      atomicAdd(ghist + (kCenter - Cfg::TB / 2) + i, (unsigned long long)v);
+    }
   }
 }
 
