@@ -181,8 +181,8 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
             d1up[c] = d1;
           }
       }
-#pragma unroll 1
       float blk2[D == 2 ? 16 : 1];   // 2D: the ZFP block is rows 1..4 of the SZ plane
+#pragma unroll 1
       for (int p = 0; p < NPL; ++p) {
         const int i = I0 + p;
         float v[5][4], h[5], d1up[4];
