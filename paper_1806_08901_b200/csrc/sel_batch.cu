@@ -163,6 +163,27 @@ __device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *m
 }
 
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned int ld_acquire_cta(const unsigned int *p) {
+  unsigned int v;
+  asm volatile("ld.acquire.cta.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(unsigned int *p, unsigned int v) {
+  asm volatile("st.release.cta.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Release requests, consumer tid 0 -> release warp (shared-memory ring).  The release warp
+// makes a flush / range publication visible (fence.acq_rel.gpu + counter increment) so the
+// fence's wait for the CTA's outstanding atomics never stalls the consumer warps.  The
+// chain consumer atomics -> bar.sync -> st.release.cta(head) -> ld.acquire.cta(head) ->
+// fence.acq_rel.gpu -> atomicAdd is cumulative (PTX memory model), so the increment
+// publishes every consumer thread's atomics.  A request never waits on another CTA.
+enum { REQ_T = 1, REQ_R = 2, REQ_END = 3 };
+struct RelReq { int kind, f; unsigned int cnt, rmin, rmax, rbad; };
+constexpr int kRelQ = 16;
+
+template <int D>
+constexpr int batch_threads() { return (TileCfg<D>::CW + 2) * 32; }   // + producer + release warp
 
 // warp 0 lane 0 spins until *flag >= target (acquire); the caller syncs the consumers
 __device__ __forceinline__ void spin_until(const unsigned int *flag, unsigned int target) {
@@ -176,7 +197,7 @@ __device__ __forceinline__ void spin_until(const unsigned int *flag, unsigned in
 }
 
 template <int D>
-__global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArgs a) {
+__global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs a) {
   using Cfg = TileCfg<D>;
   constexpr int CW = Cfg::CW;
   constexpr int NC = CW * 32;                  // consumer threads
@@ -197,6 +218,8 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   __shared__ Params s_prm;
   __shared__ int s_tbl_used;
   __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2];
+  __shared__ RelReq s_q[kRelQ];
+  __shared__ unsigned int s_qhead, s_qtail;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int grp = (int)(blockIdx.x % (unsigned)a.G);
@@ -204,6 +227,8 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   const long long ntot = (long long)nfl * (a.nR + a.nT + kFinTasks);
   if (tid == 0) {
     s_tbl_used = 0;
+    s_qhead = 0u;
+    s_qtail = 0u;
     for (int k = 0; k < 2; ++k) {
       s_rmin[k] = 0xffffffffu; s_rmax[k] = 0u; s_rbad[k] = 0u; s_rcnt[k] = 0u;
     }
@@ -213,7 +238,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
     }
     fence_barrier_init();
   }
-  for (int i = tid; i < Cfg::HIST_WORDS + Cfg::TBL_WORDS; i += Cfg::THREADS) hist[i] = 0u;
+  for (int i = tid; i < Cfg::HIST_WORDS + Cfg::TBL_WORDS; i += (int)blockDim.x) hist[i] = 0u;
   __syncthreads();
 
   // ------------------------------------------------------------------ producer
@@ -268,6 +293,44 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
     return;
   }
 
+  // ------------------------------------------------------------------ release warp
+  if (warp == CW + 1) {
+    if (lane == 0) {
+      unsigned int t = 0;
+      unsigned int ns = 32;
+      for (;;) {
+        if (t == ld_acquire_cta(&s_qhead)) {
+          __nanosleep(ns);
+          if (ns < 256) ns <<= 1;
+          continue;
+        }
+        ns = 32;
+        const RelReq r = s_q[t % kRelQ];
+        if (r.kind == REQ_END) break;
+        if (r.kind == REQ_T) {
+          fence_acq_rel_gpu();
+          atomicAdd(a.tdone + r.f, r.cnt);
+        } else {                     // REQ_R: this CTA's range slices of field r.f
+          const int g = r.f;
+          if (r.rmin != 0xffffffffu) atomicMin(a.rmin + g, r.rmin);
+          if (r.rmax != 0u) atomicMax(a.rmax + g, r.rmax);
+          if (r.rbad) atomicOr(a.rbad + g, 1u);
+          fence_acq_rel_gpu();
+          if (atomicAdd(a.rdone + g, r.cnt) + r.cnt == (unsigned)a.nR * kRWarps) {   // last
+            fence_acq_rel_gpu();
+            const float fmn = key_float(ld_acquire(a.rmin + g)), fmx = key_float(ld_acquire(a.rmax + g));
+            a.params[g] = make_params(fmn, fmx, (int)ld_acquire(a.rbad + g), a.mode, a.eb);
+            fence_acq_rel_gpu();
+            st_release(a.params_ready + g, 1u);
+          }
+        }
+        ++t;
+        st_release_cta(&s_qtail, t);
+      }
+    }
+    return;
+  }
+
   // ------------------------------------------------------------------ consumers
   unsigned int *const hlane = hist + (lane % Cfg::COPIES) * kHStride;
   unsigned int *const htrash = hist + Cfg::COPIES * kHStride;
@@ -283,34 +346,16 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
   long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // wait, flush, T, R, F, release, #flush, #publish
 #endif
 
-  // Releases are deferred: a flush / publish issues its atomics and the counter increment
-  // that makes them visible (fence + add) happens at the next task boundary, when the
-  // atomics have drained, so the fence is cheap.  Every task boundary runs the pending
-  // releases BEFORE any wait, so nobody can wait on an unreleased contribution.
-  int pend_t_field = -1;           // tid 0: tdone[pend_t_field] += pend_t_cnt pending
-  unsigned int pend_t_cnt = 0;
-  int pend_r_field = -1;           // tid 0: rdone[field] += pend_r_cnt pending
-  unsigned int pend_r_cnt = 0;
-  auto release = [&]() {
+  unsigned int qh = 0;             // tid 0: next request slot
+  auto enqueue = [&](int kind, int f, unsigned int cnt, unsigned int rmn, unsigned int rmx,
+                     unsigned int rbd) {   // tid 0 only
     const long long tp0 = PCLOCK();
-    if (tid == 0 && pend_t_field >= 0) {
-      fence_acq_rel_gpu();
-      atomicAdd(a.tdone + pend_t_field, pend_t_cnt);
-      pend_t_field = -1;
-    }
-    if (tid == 0 && pend_r_field >= 0) {
-      const int g = pend_r_field;
-      fence_acq_rel_gpu();
-      if (atomicAdd(a.rdone + g, pend_r_cnt) + pend_r_cnt == (unsigned)a.nR * kRWarps) {   // last
-
-        fence_acq_rel_gpu();
-        const float fmn = key_float(ld_acquire(a.rmin + g)), fmx = key_float(ld_acquire(a.rmax + g));
-        a.params[g] = make_params(fmn, fmx, (int)ld_acquire(a.rbad + g), a.mode, a.eb);
-        fence_acq_rel_gpu();
-        st_release(a.params_ready + g, 1u);
-      }
-      pend_r_field = -1;
-    }
+    while (qh - ld_acquire_cta(&s_qtail) >= (unsigned)kRelQ) __nanosleep(32);
+    RelReq r;
+    r.kind = kind; r.f = f; r.cnt = cnt; r.rmin = rmn; r.rmax = rmx; r.rbad = rbd;
+    s_q[qh % kRelQ] = r;
+    ++qh;
+    st_release_cta(&s_qhead, qh);
     PROF(pc[5] += clock64() - tp0);
   };
 
@@ -335,8 +380,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
     }
     if (tid == 0) {
       s_tbl_used = 0;
-      pend_t_field = cur;
-      pend_t_cnt = cur_tasks;
+      enqueue(REQ_T, cur, cur_tasks, 0u, 0u, 0u);
     }
     cur = -1;
     cur_tasks = 0;
@@ -355,11 +399,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
       const unsigned int cnt = s_rcnt[pp];
       if (cnt) {
         const int g = cur_phase * a.G + grp;                      // R(p) belongs to local field p
-        if (s_rmin[pp] != 0xffffffffu) atomicMin(a.rmin + g, s_rmin[pp]);
-        if (s_rmax[pp] != 0u) atomicMax(a.rmax + g, s_rmax[pp]);
-        if (s_rbad[pp]) atomicOr(a.rbad + g, 1u);
-        pend_r_field = g;
-        pend_r_cnt = cnt;
+        enqueue(REQ_R, g, cnt, s_rmin[pp], s_rmax[pp], s_rbad[pp]);
         PROF(pc[7] += 1);
       }
       s_rmin[pp] = 0xffffffffu;
@@ -382,17 +422,19 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1) k_batch(const BatchArg
     // flush before anything that may block (another field's tiles wait on params /
     // fin_ready, finalize waits on tdone) and at the end; range tasks never block
     const bool may_block = end || kind == KIND_F || (kind == KIND_T && f != cur);
-    release();                     // last boundary's flush / publish (their atomics drained)
     while (cur_phase < (end ? nfl + kLagF + 1 : phase)) {        // phase change(s)
       leave_phase();
       ++cur_phase;
-      release();                   // several phase changes in a row (empty phases, the end)
     }
+    // flush before anything that may block: what we hold is then handed to the release
+    // warp, which completes it without waiting on anyone
     if (cur >= 0 && may_block) flush();
-    if (may_block) release();      // about to wait: nothing of ours may stay unreleased
     const long long t_k0 = PCLOCK();
     PROF(pc[1] += t_k0 - t_w1);      // publish + flush
-    if (end) break;
+    if (end) {
+      if (tid == 0) enqueue(REQ_END, 0, 0u, 0u, 0u, 0u);
+      break;
+    }
     const float *S = base + stage * Cfg::STAGE_FLOATS;
 
     if (kind == KIND_T) {
@@ -555,7 +597,7 @@ int batch_sizes(const Geo &g, BatchSizes *bs) {
   bs->rchunk = d3 ? (TileCfg<3>::STAGE_FLOATS & ~3) : (TileCfg<2>::STAGE_FLOATS & ~3);
   bs->nR = (int)((g.N + bs->rchunk - 1) / bs->rchunk);
   bs->smem = d3 ? TileCfg<3>::SMEM : TileCfg<2>::SMEM;
-  bs->threads = d3 ? TileCfg<3>::THREADS : TileCfg<2>::THREADS;
+  bs->threads = d3 ? batch_threads<3>() : batch_threads<2>();
   bs->cw = d3 ? TileCfg<3>::CW : TileCfg<2>::CW;
   const void *fn = d3 ? batch_fn<3>() : batch_fn<2>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs->smem) != cudaSuccess)
