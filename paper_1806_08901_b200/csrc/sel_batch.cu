@@ -163,6 +163,11 @@ __device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *m
 }
 
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ float fmin_nan(float a, float b) {   // NaN if either is NaN
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
 __device__ __forceinline__ unsigned int ld_acquire_cta(const unsigned int *p) {
   unsigned int v;
   asm volatile("ld.acquire.cta.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -419,6 +424,9 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     const int4 sd = stage_desc[stage];
     const bool end = sd.x < 0;
     const int kind = end ? KIND_NONE : sd.x, f = sd.y, id = sd.z, phase = sd.w;
+    if (SEL_BATCH_PROF && a.prof && tid == 0)
+      atomicAdd(a.prof + 148 * 8 + 4 + (kind == KIND_T ? 0 : kind == KIND_R ? 1 : 2),
+                (unsigned long long)(t_w1 - t_w0));
     // flush before anything that may block (another field's tiles wait on params /
     // fin_ready, finalize waits on tdone) and at the end; range tasks never block
     const bool may_block = end || kind == KIND_F || (kind == KIND_T && f != cur);
@@ -472,23 +480,24 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       } else {
         const long long lo = (long long)id * a.rchunk;
         const int n4 = (int)min((long long)a.rchunk, a.N - lo) / 4;
+        // min propagates NaN (min.NaN), so non-finite values show up in the reduced
+        // min / max themselves: NaN -> mn is NaN, +-inf -> mx / mn infinite
         float mn = INFINITY, mx = -INFINITY;
-        int bad = 0;
 #pragma unroll 4
         for (int i = slot * 32 + lane; i < n4; i += kRWarps * 32) {
           const float4 q = reinterpret_cast<const float4 *>(S)[i];
-          bad |= is_nonfinite(q.x) | is_nonfinite(q.y) | is_nonfinite(q.z) | is_nonfinite(q.w);
-          mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
+          mn = fmin_nan(mn, fmin_nan(fmin_nan(q.x, q.y), fmin_nan(q.z, q.w)));
           mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[stage]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-          mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mn = fmin_nan(mn, __shfl_xor_sync(0xffffffffu, mn, o));
           mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          bad |= __shfl_xor_sync(0xffffffffu, bad, o);
         }
+        // (a slice with no values keeps mn = +inf > mx = -inf: not bad)
+        const int bad = (mn != mn) | ((mn <= mx) & (is_nonfinite(mn) | is_nonfinite(mx)));
         if (lane == 0) {
           const int pp = phase & 1;
           if (mn <= mx) {

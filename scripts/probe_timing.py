@@ -57,6 +57,7 @@ torch.cuda.synchronize()
 v = buf[:148 * 8].view(148, 8).double().cpu().numpy()
 q = buf[148 * 8:].double().cpu().numpy() / 148
 print("flush parts per CTA (ovf, bar1, hist, bar2):", [f"{x/1e3:.1f}k" for x in q[:4]])
+print("data wait per CTA before (T, R, F/other):", [f"{x/1e3:.1f}k" for x in q[4:7]])
 names = ["wait", "flush+publish", "T", "R", "F", "release"]
 tot = v[:, :6].sum(1)
 print("k_batch warp-0 cycles per CTA (mean):", {n: f"{v[:, k].mean()/1e3:.1f}k ({v[:, k].mean()/tot.mean()*100:.0f}%)" for k, n in enumerate(names)})
