@@ -153,6 +153,23 @@ __device__ __forceinline__ void tma_load_3d_hint(void *dst, const CUtensorMap *m
       "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch(const void *src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src),
+               "r"(bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *map, int c0, int c1,
                                                  uint64_t *bar, uint64_t policy) {
   asm volatile(
@@ -256,43 +273,66 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       uint64_t pol_keep, pol_last;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_last));
-      // the next task id is fetched one task ahead, so the atomic's round trip overlaps
-      // the wait for a free stage
-      long long next = (long long)atomicAdd(a.task_ctr + grp, 1u);
-      for (;;) {
-        const long long tau = next;
-        if (tau < ntot) next = (long long)atomicAdd(a.task_ctr + grp, 1u);
-        mbar_wait_sleep(&empty_bar[stage], ph ^ 1u);
-        int kind = KIND_NONE, f = 0, id = 0, phase = 0;
-        if (tau < ntot) {
-          decode(a, nfl, tau, kind, f, id, phase);
-          f = f * a.G + grp;                 // global field index
+      // Task ids are claimed two tasks ahead: a claimed task is decoded and its data
+      // prefetched into L2 (range chunks come from HBM; tiles of big fields too) while
+      // earlier stages are consumed; the claim's atomic itself is issued one iteration
+      // before its result is needed.
+      struct Dec { int kind, f, id, phase, btk, btj, bi; };
+      auto decode_pf = [&](long long tau, Dec &d) {
+        d.kind = KIND_NONE; d.f = 0; d.id = 0; d.phase = 0; d.btk = d.btj = d.bi = 0;
+        if (tau >= ntot) { d.kind = -1; return; }
+        decode(a, nfl, tau, d.kind, d.f, d.id, d.phase);
+        d.f = d.f * a.G + grp;             // global field index
+        if (d.kind == KIND_T) {
+          d.btk = d.id % a.tg.ntk;
+          const int rest = d.id / a.tg.ntk;
+          d.btj = rest % a.tg.ntj;
+          d.bi = rest / a.tg.ntj;
+          if constexpr (D == 3)
+            tma_prefetch_3d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1, 4 * d.bi - 1);
+          else
+            tma_prefetch_2d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1);
+        } else if (d.kind == KIND_R) {
+          const long long lo = (long long)d.id * a.rchunk;
+          const long long cnt = min((long long)a.rchunk, a.N - lo);
+          bulk_prefetch(a.xs[d.f] + lo, (uint32_t)(cnt * 4), pol_keep);
         }
-        stage_desc[stage] = make_int4(tau >= ntot ? -1 : kind, f, id, phase);
+      };
+      Dec t0, t1;
+      long long r = (long long)atomicAdd(a.task_ctr + grp, 1u);
+      decode_pf(r, t0);
+      bool more = r < ntot;
+      r = more ? (long long)atomicAdd(a.task_ctr + grp, 1u) : ntot;
+      decode_pf(r, t1);
+      more = more && r < ntot;
+      r = more ? (long long)atomicAdd(a.task_ctr + grp, 1u) : ntot;
+      for (;;) {
+        mbar_wait_sleep(&empty_bar[stage], ph ^ 1u);
+        stage_desc[stage] = make_int4(t0.kind, t0.f, t0.id, t0.phase);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
-        if (kind == KIND_T) {
-          const int btk = id % a.tg.ntk;
-          const int rest = id / a.tg.ntk;
-          const int btj = rest % a.tg.ntj;
-          const int bi = rest / a.tg.ntj;
-          stage_tile[stage] = make_int4(btk, btj, bi, 0);
+        if (t0.kind == KIND_T) {
+          stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, 0);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
-            tma_load_3d_hint(dst, a.tmaps + f, 128 * btk - 4, 4 * CW * btj - 1, 4 * bi - 1,
-                             &full_bar[stage], pol_last);
+            tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
+                             4 * t0.bi - 1, &full_bar[stage], pol_last);
           else
-            tma_load_2d_hint(dst, a.tmaps + f, 128 * btk - 4, 4 * CW * btj - 1, &full_bar[stage],
-                             pol_last);
-        } else if (kind == KIND_R) {
-          const long long lo = (long long)id * a.rchunk;
+            tma_load_2d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
+                             &full_bar[stage], pol_last);
+        } else if (t0.kind == KIND_R) {
+          const long long lo = (long long)t0.id * a.rchunk;
           const long long cnt = min((long long)a.rchunk, a.N - lo);   // multiple of 4 floats
           mbar_arrive_expect_tx(&full_bar[stage], (uint32_t)(cnt * 4));
-          bulk_load(dst, a.xs[f] + lo, (uint32_t)(cnt * 4), &full_bar[stage], pol_keep);
+          bulk_load(dst, a.xs[t0.f] + lo, (uint32_t)(cnt * 4), &full_bar[stage], pol_keep);
         } else {
-          mbar_arrive(&full_bar[stage]);   // F / padding / sentinel: no data
+          mbar_arrive(&full_bar[stage]);   // F / sentinel: no data
         }
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
-        if (tau >= ntot) break;
+        if (t0.kind < 0) break;            // the sentinel went out: done
+        t0 = t1;
+        decode_pf(r, t1);
+        more = more && r < ntot;
+        r = more ? (long long)atomicAdd(a.task_ctr + grp, 1u) : ntot;
       }
     }
     return;
