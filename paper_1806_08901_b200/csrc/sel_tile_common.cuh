@@ -10,6 +10,26 @@
 namespace sel {
 
 
+// tile configuration (developer overrides for sweeps: -DSEL_CW2=... etc.)
+#ifndef SEL_CW2
+#define SEL_CW2 24
+#endif
+#ifndef SEL_STAGES2
+#define SEL_STAGES2 3
+#endif
+#ifndef SEL_TB2
+#define SEL_TB2 8192
+#endif
+#ifndef SEL_CW3
+#define SEL_CW3 8
+#endif
+#ifndef SEL_STAGES3
+#define SEL_STAGES3 2
+#endif
+#ifndef SEL_TB3
+#define SEL_TB3 8704
+#endif
+
 constexpr int kBoxK = 4 * 32 + 4;             // 132 floats: 4 halo columns (last one used) + 128
 constexpr int kHBins = 1024;                  // histogram window: codes [-512, 512)
 constexpr int kHStride = kHBins + 1;          // copy stride (words): copy c of a bin -> bank + c
@@ -17,19 +37,19 @@ constexpr uint32_t kHOff = kSlotOff + (uint32_t)(kCenter - kHBins / 2);
 
 template <int D>
 struct TileCfg {
-  static constexpr int CW = D == 3 ? 8 : 16;                      // consumer warps
+  static constexpr int CW = D == 3 ? SEL_CW3 : SEL_CW2;           // consumer warps
   static constexpr int THREADS = (CW + 1) * 32;
   static constexpr int BOXJ = 4 * CW + 1;                         // halo row + 4 per warp
   static constexpr int BOXI = D == 3 ? 5 : 1;                     // halo plane + 4 (3D)
   static constexpr int PLANE = kBoxK * BOXJ;                      // floats per smem plane
   static constexpr uint32_t STAGE_BYTES = PLANE * BOXI * 4;
   static constexpr int STAGE_FLOATS = ((STAGE_BYTES + 127) & ~127) / 4;
-  static constexpr int STAGES = D == 3 ? 2 : 4;
+  static constexpr int STAGES = D == 3 ? SEL_STAGES3 : SEL_STAGES2;
   static constexpr int COPIES = D == 3 ? 4 : 8;                   // histogram lane copies
   static constexpr int HIST_WORDS = (COPIES + 1) * kHStride;   // + trash copy
   // second level: one table of TB 32-bit counters centred on code 0 for the codes
   // outside the lane-copy window (wide distributions: noise, fronts, coarse data)
-  static constexpr int TB = D == 3 ? 8704 : 13696;    // leaves ~2.5 KB of the SM for k_minmax + k_finalize
+  static constexpr int TB = D == 3 ? SEL_TB3 : SEL_TB2;
   static constexpr int TBL_WORDS = TB;
   static constexpr uint32_t kTOff = kSlotOff + (uint32_t)(kCenter - TB / 2);   // bits -> table slot
   static constexpr size_t SMEM = 128 + (size_t)STAGES * STAGE_FLOATS * 4 + HIST_WORDS * 4 +

@@ -5,14 +5,14 @@ import torch
 import paper_1806_08901_b200 as sel
 import synth
 
-for cfg, nf in ((2, 100), (3, 10), (1, 256)):
+for cfg, nf in (((2, 100), (3, 10), (1, 256)) if len(sys.argv) < 2 else [tuple(map(int, a.split(":"))) for a in sys.argv[1:]]):
     shape = synth.CONFIGS[cfg]["shape"]
     fields = [torch.from_numpy(synth.make_field(cfg, i)).cuda() for i in range(nf)]
     eb = synth.CONFIGS[cfg]["eb_rel"][0]
     p = sel.Plan(shape, eb, "rel")
     buf = p.results_buffer(nf)
     ref = None
-    for G in ((0, 1, 2, 3, 4) if cfg != 1 else (0, 4, 8, 12, 16, 24)):
+    for G in (((0, 1, 2, 3, 4) if cfg != 1 else (0, 4, 8, 12, 16, 24)) if os.environ.get("SWEEP_G") else (0,)):
         if G > nf:
             continue
         p.set_option("groups", G)
