@@ -231,14 +231,24 @@ __device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int mi
   //   GT = sum_j max(0, S_j-kmin+1)                = sum_j Q_j - SZ (kmin-1)
   //      + #{j : f_j >= kmin and f_j >= S_{j+1}}   (f_j >= kmin and f_j >= Q_{j+1})
   //      + 32 - max(f_L+1, kmin) - [f_L >= kmin]
-    int Q = kmin - 1, t1 = 0, t2 = 0;
+  // evaluated with R_j = max(kmin, S_j): the middle set is C = {j : f_j >= R_{j+1}}
+  // (a bit mask, counted by popc), and sum_j Q_j = sum_j R_j - z with z = #{j : S_j <
+  // kmin} = SZ-1-max(C) (the highest j of C is the last significant coefficient).
+    int R = kmin, sR = 0;
+    uint32_t cm0 = 0u, cm1 = 0u;   // C for j < 32 / j >= 32
 #pragma unroll
     for (int j = SZ - 1; j >= 0; --j) {
       const int f = flo(u[j]);
-      t2 += (f >= kmin && f >= Q) ? 1 : 0;
-      Q = max(Q, f);
-      t1 += Q;
+      if (f >= R) {
+        if (j < 32) cm0 |= 1u << (j & 31);
+        else cm1 |= 1u << (j & 31);
+      }
+      R = max(R, f);
+      sR += R;
     }
+    const int last = cm1 ? 32 + flo(cm1) : flo(cm0);       // -1 if C is empty
+    const int t1 = sR - (SZ - 1 - last);
+    const int t2 = __popc(cm0) + __popc(cm1);
     const int fL = flo(u[SZ - 1]);
     const int t3 = 32 - max(fL + 1, kmin) - (fL >= kmin ? 1 : 0);
     bits = (uint32_t)(9 + t1 - SZ * (kmin - 1) + t2 + t3);
