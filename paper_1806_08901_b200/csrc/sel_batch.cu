@@ -237,7 +237,6 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   int4 *const stage_tile = stage_desc + Cfg::STAGES;
   __shared__ double s_red[3][CW];
   __shared__ unsigned long long s_redu[2][CW];
-  __shared__ Params s_prm;
   __shared__ int s_tbl_used;
   __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2];
   __shared__ RelReq s_q[kRelQ];
@@ -277,11 +276,12 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       // prefetched into L2 (range chunks come from HBM; tiles of big fields too) while
       // earlier stages are consumed; the claim's atomic itself is issued one iteration
       // before its result is needed.
-      struct Dec { int kind, f, id, phase, btk, btj, bi; };
+      struct Dec { int kind, f, id, phase, btk, btj, bi, slot; };
       auto decode_pf = [&](long long tau, Dec &d) {
-        d.kind = KIND_NONE; d.f = 0; d.id = 0; d.phase = 0; d.btk = d.btj = d.bi = 0;
+        d.kind = KIND_NONE; d.f = 0; d.id = 0; d.phase = 0; d.btk = d.btj = d.bi = 0; d.slot = 0;
         if (tau >= ntot) { d.kind = -1; return; }
         decode(a, nfl, tau, d.kind, d.f, d.id, d.phase);
+        d.slot = grp * kRing + d.f % kRing;  // = ring(a, global field)
         d.f = d.f * a.G + grp;             // global field index
         if (d.kind == KIND_T) {
           d.btk = d.id % a.tg.ntk;
@@ -309,9 +309,9 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       for (;;) {
         mbar_wait_sleep(&empty_bar[stage], ph ^ 1u);
         stage_desc[stage] = make_int4(t0.kind, t0.f, t0.id, t0.phase);
+        stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, t0.slot);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
         if (t0.kind == KIND_T) {
-          stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, 0);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
             tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
@@ -380,6 +380,8 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   unsigned int *const hlane = hist + (lane % Cfg::COPIES) * kHStride;
   unsigned int *const htrash = hist + Cfg::COPIES * kHStride;
   int cur = -1;                    // field owning the smem histogram
+  int cur_slot = 0;                // its ring slot
+  int flush_mark = 1;              // flush interval number (s_tbl_used starts at 0)
   unsigned int cur_tasks = 0;      // its T tasks since the last flush
   unsigned int ovf = 0;
   bool ok = false;
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   };
 
   auto flush = [&]() {             // all consumers, same task: move smem histogram to global
-    unsigned long long *gh = a.hist + (size_t)ring(a, cur) * kNSlots;
+    unsigned long long *gh = a.hist + (size_t)cur_slot * kNSlots;
     const long long q0 = PCLOCK();
     ovf_flush(ovf, gh);
     ovf = 0;
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     consumer_sync<NC>();
     const long long q2 = PCLOCK();
     PROF(pc[6] += 1);
-    tile_hist_flush<D>(hist, tbl, &s_tbl_used, gh, tid, NC);
+    tile_hist_flush<D>(hist, tbl, &s_tbl_used, flush_mark, gh, tid, NC);
     const long long q3 = PCLOCK();
     consumer_sync<NC>();           // every consumer's atomics issued before the release
     const long long q4 = PCLOCK();
@@ -423,10 +425,8 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       atomicAdd(a.prof + 148 * 8 + 2, (unsigned long long)(q3 - q2));
       atomicAdd(a.prof + 148 * 8 + 3, (unsigned long long)(q4 - q3));
     }
-    if (tid == 0) {
-      s_tbl_used = 0;
-      enqueue(REQ_T, cur, cur_tasks, 0u, 0u, 0u);
-    }
+    ++flush_mark;                  // codes from now on mark the table with the next interval
+    if (tid == 0) enqueue(REQ_T, cur, cur_tasks, 0u, 0u, 0u);
     cur = -1;
     cur_tasks = 0;
   };
@@ -486,29 +486,30 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     const float *S = base + stage * Cfg::STAGE_FLOATS;
 
     if (kind == KIND_T) {
-      if (cur < 0) {               // first tile of field f here: params, parity buffer free
-        if (tid == 0) {
+      const int4 tc = stage_tile[stage];
+      if (cur < 0) {               // first tile of field f here: params, ring slot free
+        // per warp (no CTA barrier): lane 0 acquires the flags, the warp barrier orders
+        // the lanes' L2 reads (ld.cg: never a stale L1 line) after it
+        if (lane == 0) {
           spin_until(a.params_ready + f, 1u);
           if (f >= kRing * a.G) spin_until(a.fin_ready + f - kRing * a.G, 1u);   // slot's last user
-          s_prm = a.params[f];
         }
-        consumer_sync<NC>();
-        const Params prm = s_prm;
-        ok = prm.status == SEL_OK;
-        r_f = prm.r_f;
-        minexp = prm.minexp;
+        __syncwarp();
+        ok = __ldcg(&a.params[f].status) == SEL_OK;
+        r_f = __ldcg(&a.params[f].r_f);
+        minexp = __ldcg(&a.params[f].minexp);
         cur = f;
+        cur_slot = tc.w;
       }
       uint64_t tbits = 0;
       double terr = 0.0;
-      const int4 tc = stage_tile[stage];
       tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hlane, htrash,
-                             tbl, &s_tbl_used, a.hist + (size_t)ring(a, f) * kNSlots, ovf, nodbg,
+                             tbl, &s_tbl_used, flush_mark, a.hist + (size_t)tc.w * kNSlots, ovf, nodbg,
                              tbits, terr);
       ++cur_tasks;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
-      task_store(a.tpart + (size_t)ring(a, f) * a.nT * CW, id * CW + warp, tbits, terr);
+      task_store(a.tpart + (size_t)tc.w * a.nT * CW, id * CW + warp, tbits, terr);
     } else if (kind == KIND_R) {
       // ---- min / max / non-finite of the staged chunk (R1) by kRWarps consumer warps
       // (rotating with the task id); the others release the stage at once and move on.
@@ -549,13 +550,14 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         }
       }
     } else if (kind == KIND_F) {
+      const int slot = stage_tile[stage].w;   // read before the stage is released
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
       if (tid == 0) spin_until(a.tdone + f, (unsigned)a.nT);
       consumer_sync<NC>();
-      unsigned long long *gh = a.hist + (size_t)ring(a, f) * kNSlots;
-      const Partial *tpf = a.tpart + (size_t)ring(a, f) * a.nT * CW;
-      FPart *fpf = a.fpart + (size_t)ring(a, f) * kFinTasks;
+      unsigned long long *gh = a.hist + (size_t)slot * kNSlots;
+      const Partial *tpf = a.tpart + (size_t)slot * a.nT * CW;
+      FPart *fpf = a.fpart + (size_t)slot * kFinTasks;
       // ---- 1/8 of the histogram: sum c log2(N/c), re-zero; and 1/8 of the tile partials
       const double Nsz = (double)a.fa.n_sz;
       const double lN = log2(Nsz);

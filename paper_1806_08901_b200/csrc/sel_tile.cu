@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
     uint64_t tbits = 0;
     double terr = 0.0;
     tile_consume<D, DBG>(S, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hlane, htrash, tbl,
-                         &s_tbl_used, ws.hist, ovf, dbg, tbits, terr);
+                         &s_tbl_used, 1, ws.hist, ovf, dbg, tbits, terr);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[stage]);      // stage free for the producer
     task_store(ws.task_part, t * CW + warp, tbits, terr);
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
   }
   ovf_flush(ovf, ws.hist);
   consumer_sync<CW * 32>();
-  tile_hist_flush<D>(hist, tbl, &s_tbl_used, ws.hist, threadIdx.x, CW * 32);
+  tile_hist_flush<D>(hist, tbl, &s_tbl_used, 1, ws.hist, threadIdx.x, CW * 32);
 }
 
 // ============================================================ host side

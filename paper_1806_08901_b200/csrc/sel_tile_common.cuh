@@ -161,7 +161,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
                                              const TileGeo &tg, int warp,
                                              int lane, bool ok, float r_f, int minexp,
                                              unsigned int *hlane, unsigned int *htrash,
-                                             unsigned int *tbl, int *tbl_used,
+                                             unsigned int *tbl, int *tbl_used, int tbl_mark,
                                              unsigned long long *ghist,
                                              unsigned int &ovf, const DebugPtrs &dbg,
                                              uint64_t &tbits, double &terr) {
@@ -265,7 +265,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
               if (out && tb < (uint32_t)Cfg::TB) atomicAdd(tbl + tb, 1u);
               far |= (out && tb >= (uint32_t)Cfg::TB) ? (1u << c) : 0u;
             }
-            if (lane == 0) *tbl_used = 1;
+            if (lane == 0) *tbl_used = tbl_mark;
             if (__any_sync(0xffffffffu, far != 0u)) {
 #pragma unroll
               for (int c = 0; c < 4; ++c)
@@ -321,7 +321,8 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
 // and clear it.  Called by the consumer threads (tid < nthr) after a consumer barrier.
 template <int D>
 __device__ __forceinline__ void tile_hist_flush(unsigned int *hist, unsigned int *tbl,
-                                                const int *tbl_used, unsigned long long *ghist,
+                                                const int *tbl_used, int tbl_mark,
+                                                unsigned long long *ghist,
                                                 int tid, int nthr) {
   using Cfg = TileCfg<D>;
   for (int i = tid; i < kHBins; i += nthr) {
@@ -333,7 +334,9 @@ __device__ __forceinline__ void tile_hist_flush(unsigned int *hist, unsigned int
     }
     if (c) atomicAdd(ghist + (kCenter - kHBins / 2) + i, c);
   }
-  if (!*tbl_used) return;               // no code outside the lane-copy window: table is zero
+  // the flag holds the mark of the last flush interval that used the table (a mark per
+  // interval, so nobody has to reset it between a flush and the next codes)
+  if (*tbl_used != tbl_mark) return;    // no code outside the lane-copy window: table is zero
   for (int i = tid; i < Cfg::TB; i += nthr) {
     const uint32_t v = tbl[i];
     if (v) {
