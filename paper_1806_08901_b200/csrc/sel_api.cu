@@ -55,6 +55,7 @@ struct sel_plan_st {
   BatchSizes bs{};                                // persistent batch kernel sizes
   int use_batch = 1;
   int groups = 0;                 // k_batch CTA groups (0: auto, batch_groups)
+  int lag_t = 2;                  // k_batch phases from a field's range pass to its tiles
   void *bstate = nullptr;                         // batch kernel state (grows with n)
   cudaEvent_t bev[2] = {nullptr, nullptr};        // kernel_timing around k_batch
   bool batch_timed = false;
@@ -251,7 +252,7 @@ int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
     }
   }
   int rc = launch_batch(g, p->tl[0], p->bs, x, n, p->bstate, p->bstate_cap, fa, p->mode, p->eb,
-                        p->d_res, p->sm_count, G, st, p->timing ? p->bev : nullptr);
+                        p->d_res, p->sm_count, G, p->lag_t, st, p->timing ? p->bev : nullptr);
   if (rc) return cuda_fail(cudaGetLastError(), "k_batch launch");
   p->launches += 1;
   p->batch_timed = p->timing;
@@ -505,6 +506,11 @@ int sel_set_option(sel_plan_t p, const char *key, double value) {
   if (!strcmp(key, "debug")) {
     p->debug = value != 0.0;
     if (p->debug) return ensure_debug(p);
+    return SEL_OK;
+  }
+  if (!strcmp(key, "lag")) {
+    if (!(value >= 1.0 && value <= 4.0)) return SEL_EINVAL;
+    p->lag_t = (int)value;
     return SEL_OK;
   }
   if (!strcmp(key, "groups")) {

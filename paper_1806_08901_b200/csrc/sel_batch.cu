@@ -26,7 +26,7 @@ namespace sel {
 
 constexpr int kFinTasks = 8;                   // F tasks per field (8192 slots each)
 constexpr int kRing = 3;                       // histogram / partial buffers (field % 3)
-constexpr int kLagT = 2, kLagF = 4;            // phase p: R(p), T(p - kLagT), F(p - kLagF)
+// phase p: R(p), T(p - lagT), F(p - lagF) with lagF = lagT + 2 (BatchArgs; default 2 / 4)
 constexpr int kRWarps = 2;                     // consumer warps reducing one range chunk
 #ifndef SEL_BATCH_PROF
 #define SEL_BATCH_PROF 0                       // 1: per-CTA cycle counters (sel_dev_batch_profile)
@@ -69,6 +69,7 @@ struct BatchArgs {
   unsigned int *tdone;            // [nf] tile tasks whose histogram counts are flushed
   unsigned int *fdone;            // [nf]
   unsigned int *fin_ready;        // [nf]
+  int lagT, lagF;                 // phases from a field's range pass to its tiles / finalize
   int G;                          // CTA groups: group g = blockIdx % G runs fields f = g (mod G)
   unsigned long long *hist;       // [G * kRing][kNSlots], slot ring(f)
   Partial *tpart;                 // [G * kRing][nT * CW]
@@ -89,8 +90,8 @@ enum { KIND_NONE = 0, KIND_R = 1, KIND_T = 2, KIND_F = 3 };
 __device__ __forceinline__ bool in_range(int nfl, int f) { return f >= 0 && f < nfl; }
 
 __device__ __forceinline__ long long phase_size(const BatchArgs &a, int nfl, int p) {
-  return (long long)(in_range(nfl, p - kLagF) ? kFinTasks : 0) + (in_range(nfl, p) ? a.nR : 0) +
-         (in_range(nfl, p - kLagT) ? a.nT : 0);
+  return (long long)(in_range(nfl, p - a.lagF) ? kFinTasks : 0) + (in_range(nfl, p) ? a.nR : 0) +
+         (in_range(nfl, p - a.lagT) ? a.nT : 0);
 }
 
 // buffer slot of field f: kRing per group, reused by field f + kRing * G
@@ -100,21 +101,21 @@ __device__ __forceinline__ int ring(const BatchArgs &a, int f) {
 
 __device__ __forceinline__ void decode(const BatchArgs &a, int nfl, long long tau, int &kind, int &f,
                                        int &id, int &phase) {
-  // phases 0 .. kLagF-1 are the ramp, kLagF .. nfl-1 share one size, then the tail
+  // phases 0 .. a.lagF-1 are the ramp, a.lagF .. nfl-1 share one size, then the tail
   int p = 0;
   long long m = tau;
-  const int ramp_end = nfl < kLagF ? nfl : kLagF;
+  const int ramp_end = nfl < a.lagF ? nfl : a.lagF;
   for (; p < ramp_end; ++p) {
     const long long sz = phase_size(a, nfl, p);
     if (m < sz) break;
     m -= sz;
   }
   if (p == ramp_end) {
-    const int nmid = nfl > kLagF ? nfl - kLagF : 0;
+    const int nmid = nfl > a.lagF ? nfl - a.lagF : 0;
     const long long S = (long long)kFinTasks + a.nR + a.nT;
     if (nmid > 0 && m < nmid * S) {
       const int q = (int)(m / S);
-      p = kLagF + q;
+      p = a.lagF + q;
       m -= (long long)q * S;
     } else {
       m -= (long long)nmid * S;
@@ -123,17 +124,17 @@ __device__ __forceinline__ void decode(const BatchArgs &a, int nfl, long long ta
     }
   }
   phase = p;
-  const int nF = in_range(nfl, p - kLagF) ? kFinTasks : 0;
+  const int nF = in_range(nfl, p - a.lagF) ? kFinTasks : 0;
   if (m < nF) {
-    kind = KIND_F; f = p - kLagF; id = (int)m;
+    kind = KIND_F; f = p - a.lagF; id = (int)m;
     return;
   }
   m -= nF;
-  const long long nRp = in_range(nfl, p) ? a.nR : 0, nTp = in_range(nfl, p - kLagT) ? a.nT : 0;
+  const long long nRp = in_range(nfl, p) ? a.nR : 0, nTp = in_range(nfl, p - a.lagT) ? a.nT : 0;
   const long long M = nRp + nTp;
   const long long r0 = m * nRp / M, r1 = (m + 1) * nRp / M;
   if (r1 > r0) { kind = KIND_R; f = p; id = (int)r0; }
-  else { kind = KIND_T; f = p - kLagT; id = (int)(m - r0); }
+  else { kind = KIND_T; f = p - a.lagT; id = (int)(m - r0); }
 }
 
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     // flush before anything that may block (another field's tiles wait on params /
     // fin_ready, finalize waits on tdone) and at the end; range tasks never block
     const bool may_block = end || kind == KIND_F || (kind == KIND_T && f != cur);
-    while (cur_phase < (end ? nfl + kLagF + 1 : phase)) {        // phase change(s)
+    while (cur_phase < (end ? nfl + a.lagF + 1 : phase)) {        // phase change(s)
       leave_phase();
       ++cur_phase;
     }
@@ -665,8 +666,9 @@ size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G) {
 
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
-                 sel_result *d_results, int sm_count, int G, cudaStream_t st, cudaEvent_t *ev) {
-  if (G < 1 || G > nf || G > sm_count) return SEL_EINVAL;
+                 sel_result *d_results, int sm_count, int G, int lagT, cudaStream_t st,
+                 cudaEvent_t *ev) {
+  if (G < 1 || G > nf || G > sm_count || lagT < 1 || lagT > 4) return SEL_EINVAL;
   // state layout (device): tmaps | xs | params | counters | hist x2 | tpart x2 | fpart x2
   char *b = (char *)state;
   size_t off = 0;
@@ -724,6 +726,8 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   a.rbad = ctrs + 7 * nf;
   a.task_ctr = ctrs + 8 * nf;
   a.G = G;
+  a.lagT = lagT;
+  a.lagF = lagT + 2;
   a.hist = hst;
   a.tpart = tp;
   a.fpart = fp;

@@ -136,7 +136,8 @@ int batch_sizes(const Geo &g, BatchSizes *bs);
 size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G);
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
-                 sel_result *d_results, int sm_count, int G, cudaStream_t st, cudaEvent_t *ev);
+                 sel_result *d_results, int sm_count, int G, int lagT, cudaStream_t st,
+                 cudaEvent_t *ev);
 int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl);
 int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Workspace &ws,
                 const DebugPtrs *dbg, cudaStream_t st);

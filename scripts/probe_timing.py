@@ -11,6 +11,8 @@ shape = synth.CONFIGS[cfg]["shape"]
 fields = [torch.from_numpy(synth.make_field(cfg, i)).cuda() for i in range(nf)]
 eb = synth.CONFIGS[cfg]["eb_rel"][0]
 p = sel.Plan(shape, eb, "rel")
+if os.environ.get("SEL_G"):
+    p.set_option("groups", int(os.environ["SEL_G"]))
 
 def timeit(fn, reps=5):
     fn(); torch.cuda.synchronize()
