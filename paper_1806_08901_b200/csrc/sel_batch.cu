@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       for (;;) {
         if (t == ld_acquire_cta(&s_qhead)) {
           __nanosleep(ns);
-          if (ns < 256) ns <<= 1;
+          if (ns < 2048) ns <<= 1;        // requests are rare; polling steals issue slots
           continue;
         }
         ns = 32;
