@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   unsigned int *const tbl = hist + Cfg::HIST_WORDS;
   // barriers + per-stage descriptors, 16-byte aligned (hist starts 128-byte aligned)
   uint64_t *const full_bar =
-      reinterpret_cast<uint64_t *>(hist + Cfg::BAR_OFF);
+      reinterpret_cast<uint64_t *>(hist + ((Cfg::HIST_WORDS + Cfg::TBL_WORDS + 3) & ~3));
   uint64_t *const empty_bar = full_bar + Cfg::STAGES;
   // per stage, decoded once by the producer: {kind | end flag, f, id, phase} and the tile
   // coordinates {btk, btj, bi}
@@ -290,9 +290,9 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
           d.btj = rest % a.tg.ntj;
           d.bi = rest / a.tg.ntj;
           if constexpr (D == 3)
-            tma_prefetch_3d(a.tmaps + d.f, 128 * d.btk - 4, Cfg::ROWS * d.btj - 1, 4 * d.bi - 1);
+            tma_prefetch_3d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1, 4 * d.bi - 1);
           else
-            tma_prefetch_2d(a.tmaps + d.f, 128 * d.btk - 4, Cfg::ROWS * d.btj - 1);
+            tma_prefetch_2d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1);
         } else if (d.kind == KIND_R) {
           const long long lo = (long long)d.id * a.rchunk;
           const long long cnt = min((long long)a.rchunk, a.N - lo);
@@ -315,10 +315,10 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         if (t0.kind == KIND_T) {
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
-            tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, Cfg::ROWS * t0.btj - 1,
+            tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
                              4 * t0.bi - 1, &full_bar[stage], pol_last);
           else
-            tma_load_2d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, Cfg::ROWS * t0.btj - 1,
+            tma_load_2d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
                              &full_bar[stage], pol_last);
         } else if (t0.kind == KIND_R) {
           const long long lo = (long long)t0.id * a.rchunk;
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       double terr = 0.0;
       tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hlane, htrash,
                              tbl, &s_tbl_used, flush_mark, a.hist + (size_t)tc.w * kNSlots, ovf, nodbg,
-                             hist + Cfg::SCR_OFF + warp * kScrWarp, tbits, terr);
+                             tbits, terr);
       ++cur_tasks;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);

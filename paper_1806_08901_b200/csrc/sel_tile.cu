@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
   unsigned int *const tbl = hist + Cfg::HIST_WORDS;
   // barriers + per-stage descriptors, 16-byte aligned (hist starts 128-byte aligned)
   uint64_t *const full_bar =
-      reinterpret_cast<uint64_t *>(hist + Cfg::BAR_OFF);
+      reinterpret_cast<uint64_t *>(hist + ((Cfg::HIST_WORDS + Cfg::TBL_WORDS + 3) & ~3));
   uint64_t *const empty_bar = full_bar + Cfg::STAGES;
   int4 *const stage_task = reinterpret_cast<int4 *>(empty_bar + Cfg::STAGES);   // {t, btk, btj, bi}
 
@@ -74,9 +74,9 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
         float *dst = base + stage * Cfg::STAGE_FLOATS;
         mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
         if constexpr (D == 3)
-          tma_load_3d(dst, &tmap, 128 * btk - 4, Cfg::ROWS * btj - 1, 4 * bi - 1, &full_bar[stage]);
+          tma_load_3d(dst, &tmap, 128 * btk - 4, 4 * CW * btj - 1, 4 * bi - 1, &full_bar[stage]);
         else
-          tma_load_2d(dst, &tmap, 128 * btk - 4, Cfg::ROWS * btj - 1, &full_bar[stage]);
+          tma_load_2d(dst, &tmap, 128 * btk - 4, 4 * CW * btj - 1, &full_bar[stage]);
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
       }
     }
@@ -102,8 +102,7 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
     uint64_t tbits = 0;
     double terr = 0.0;
     tile_consume<D, DBG>(S, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hlane, htrash, tbl,
-                         &s_tbl_used, 1, ws.hist, ovf, dbg,
-                         hist + Cfg::SCR_OFF + warp * kScrWarp, tbits, terr);
+                         &s_tbl_used, 1, ws.hist, ovf, dbg, tbits, terr);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[stage]);      // stage free for the producer
     task_store(ws.task_part, t * CW + warp, tbits, terr);
@@ -143,9 +142,8 @@ bool tile_supported(const Geo &g) {
 int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl) {
   TileGeo &t = tl->tg;
   const int cw = g.ndims == 3 ? TileCfg<3>::CW : TileCfg<2>::CW;
-  const int wj = g.ndims == 3 ? TileCfg<3>::WJ : TileCfg<2>::WJ;   // block rows per tile
   for (int a = 0; a < 3; ++a) { t.n[a] = g.n[a]; t.nb[a] = (int)g.nb[a]; }
-  t.ntj = (int)((g.nb[1] + wj - 1) / wj);
+  t.ntj = (int)((g.nb[1] + cw - 1) / cw);
   t.ntk = (int)((g.nb[2] + 31) / 32);
   const int64_t nt = (int64_t)t.ntj * t.ntk * (g.ndims == 3 ? g.nb[0] : 1);
   if (nt > (1LL << 26)) return SEL_EINVAL;

@@ -21,13 +21,13 @@ namespace sel {
 #define SEL_TB2 8192
 #endif
 #ifndef SEL_CW3
-#define SEL_CW3 16
+#define SEL_CW3 8
 #endif
 #ifndef SEL_STAGES3
-#define SEL_STAGES3 3
+#define SEL_STAGES3 2
 #endif
 #ifndef SEL_TB3
-#define SEL_TB3 6144
+#define SEL_TB3 8704
 #endif
 
 constexpr int kBoxK = 4 * 32 + 4;             // 132 floats: 4 halo columns (last one used) + 128
@@ -39,10 +39,7 @@ template <int D>
 struct TileCfg {
   static constexpr int CW = D == 3 ? SEL_CW3 : SEL_CW2;           // consumer warps
   static constexpr int THREADS = (CW + 1) * 32;
-  // block rows per tile: one per warp (2D), CW / 4 (3D: 4 warps along k, 4 lanes per block)
-  static constexpr int WJ = D == 3 ? CW / 4 : CW;
-  static constexpr int ROWS = 4 * WJ;                             // field rows per tile
-  static constexpr int BOXJ = ROWS + 1;                           // + halo row
+  static constexpr int BOXJ = 4 * CW + 1;                         // halo row + 4 per warp
   static constexpr int BOXI = D == 3 ? 5 : 1;                     // halo plane + 4 (3D)
   static constexpr int PLANE = kBoxK * BOXJ;                      // floats per smem plane
   static constexpr uint32_t STAGE_BYTES = PLANE * BOXI * 4;
@@ -55,13 +52,8 @@ struct TileCfg {
   static constexpr int TB = D == 3 ? SEL_TB3 : SEL_TB2;
   static constexpr int TBL_WORDS = TB;
   static constexpr uint32_t kTOff = kSlotOff + (uint32_t)(kCenter - TB / 2);   // bits -> table slot
-  // 3D: per-warp scratch for the 4-lane block exchanges (sel_tile3q.cuh), then barriers
-  static constexpr int SCR_OFF = (HIST_WORDS + TBL_WORDS + 3) & ~3;      // words from hist
-  static constexpr int SCR_WORDS = D == 3 ? CW * 640 : 0;
-  static constexpr int BAR_OFF = SCR_OFF + SCR_WORDS;
-  static constexpr size_t SMEM = 128 + (size_t)STAGES * STAGE_FLOATS * 4 + (size_t)BAR_OFF * 4 +
-                                 STAGES * 48 + 16;
-  static_assert(D != 3 || CW % 4 == 0, "3D tiles are 4 warps wide");
+  static constexpr size_t SMEM = 128 + (size_t)STAGES * STAGE_FLOATS * 4 + HIST_WORDS * 4 +
+                                 TBL_WORDS * 4 + STAGES * 48 + 16;
 };
 
 // ------------------------------------------------------------ mbarrier / TMA PTX
@@ -161,10 +153,6 @@ __device__ __forceinline__ uint32_t sz_win(float d, float r_f, unsigned int *hco
 }
 
 
-}  // namespace sel
-#include "sel_tile3q.cuh"
-namespace sel {
-
 // Consumer work of one tile task (block-layer bi, tile row btj, tile column btk; warp-level:
 // every consumer warp of the CTA calls it for the same tile).  S: the tile's smem stage.  Adds the SZ codes to the CTA's histogram
 // (lane copies / packed table / ghist / ovf) and returns the lane's block bits/error.
@@ -176,12 +164,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
                                              unsigned int *tbl, int *tbl_used, int tbl_mark,
                                              unsigned long long *ghist,
                                              unsigned int &ovf, const DebugPtrs &dbg,
-                                             unsigned int *scr, uint64_t &tbits, double &terr) {
-  if constexpr (D == 3) {
-    tile_consume_3q<DBG, TileCfg<3>::TB>(S, btk, btj, bi, tg, warp, lane, ok, r_f, minexp, hlane, htrash, tbl,
-                              tbl_used, tbl_mark, ghist, ovf, dbg, scr, tbits, terr);
-    return;
-  }
+                                             uint64_t &tbits, double &terr) {
   using Cfg = TileCfg<D>;
   constexpr int CW = Cfg::CW;
   constexpr int SZ = Tab<D>::SIZE;
