@@ -51,6 +51,7 @@ struct sel_plan_st {
   int mm_ctas = 0;
   EstLaunch el[2][2] = {};                        // [vec][debug]
   bool tile_ok = false;                           // TMA tile path available for this shape
+  bool sampled_ok = false;                        // k_batch sampled-block tasks available
   TileLaunch tl[2] = {};                          // [debug]
   BatchSizes bs{};                                // persistent batch kernel sizes
   int use_batch = 1;
@@ -200,7 +201,7 @@ int enqueue_est(sel_plan_t p, const float *x, int f, cudaStream_t st, TimingSlot
 // One persistent launch for the whole batch (sel_batch.cu): value range, tiles and
 // finalize of every field as one task stream; results land in d_res[0..n).
 bool batch_ok(sel_plan_t p, const float *const *x, int n) {
-  if (!p->tile_ok || !p->use_batch || p->debug) return false;
+  if (!(p->tile_ok || p->sampled_ok) || !p->use_batch || p->debug) return false;
   for (int f = 0; f < n; ++f)
     if (((uintptr_t)x[f] & 15u) != 0) return false;
   return true;
@@ -224,7 +225,7 @@ int batch_groups(sel_plan_t p, int n) {
 
 int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
   const int G = batch_groups(p, n);
-  const size_t need = batch_state_bytes(n, p->bs, p->tl[0].tg.ntasks, G);
+  const size_t need = batch_state_bytes(n, p->bs, batch_ntasks(p->geo, p->tl[0], p->bs), G);
   if (need > p->bstate_cap) {
     if (p->bstate) {
       CK(cudaStreamSynchronize(st));
@@ -443,7 +444,10 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double e
     }
     if (p->tl[d].npart > p->max_tasks) p->max_tasks = p->tl[d].npart;
   }
-  if (p->tile_ok && batch_sizes(g, &p->bs) != SEL_OK) {
+  // sampled strides: k_batch runs one processed block per lane (2D/3D, float4 rows)
+  p->sampled_ok = (g.ndims == 2 || g.ndims == 3) && (g.s[0] > 1 || g.s[1] > 1 || g.s[2] > 1) &&
+                  g.n[2] % 4 == 0 && g.n_pb < (1LL << 31);
+  if ((p->tile_ok || p->sampled_ok) && batch_sizes(g, &p->bs) != SEL_OK) {
     cuda_fail(cudaGetLastError(), "batch_sizes");
     delete p;
     return SEL_ECUDA;

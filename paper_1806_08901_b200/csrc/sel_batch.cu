@@ -55,6 +55,8 @@ struct BatchArgs {
   const float *const *xs;         // [nf] device pointers
   int nf;
   TileGeo tg;
+  Geo g;                          // sampling geometry (sampled != 0: strides > 1)
+  int sampled;                    // T tasks are sampled-block tasks (no TMA tile)
   int64_t N;
   int nR, nT, phase;              // tasks per field (F: kFinTasks); phase = kFinTasks + nR + nT
   int rchunk;                     // floats per R task
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         decode(a, nfl, tau, d.kind, d.f, d.id, d.phase);
         d.slot = grp * kRing + d.f % kRing;  // = ring(a, global field)
         d.f = d.f * a.G + grp;             // global field index
-        if (d.kind == KIND_T) {
+        if (d.kind == KIND_T && !a.sampled) {
           d.btk = d.id % a.tg.ntk;
           const int rest = d.id / a.tg.ntk;
           d.btj = rest % a.tg.ntj;
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         stage_desc[stage] = make_int4(t0.kind, t0.f, t0.id, t0.phase);
         stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, t0.slot);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
-        if (t0.kind == KIND_T) {
+        if (t0.kind == KIND_T && !a.sampled) {
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
             tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
           mbar_arrive_expect_tx(&full_bar[stage], (uint32_t)(cnt * 4));
           bulk_load(dst, a.xs[t0.f] + lo, (uint32_t)(cnt * 4), &full_bar[stage], pol_keep);
         } else {
-          mbar_arrive(&full_bar[stage]);   // F / sentinel: no data
+          mbar_arrive(&full_bar[stage]);   // F / sampled T / sentinel: no staged data
         }
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
         if (t0.kind < 0) break;            // the sentinel went out: done
@@ -504,9 +506,16 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       }
       uint64_t tbits = 0;
       double terr = 0.0;
-      tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hlane, htrash,
-                             tbl, &s_tbl_used, flush_mark, a.hist + (size_t)tc.w * kNSlots, ovf, nodbg,
-                             tbits, terr);
+      if (a.sampled) {             // processed blocks id*NC .. +NC-1, one per consumer lane
+        const int64_t t = ((int64_t)id * CW + warp) * 32 + lane;
+        sampled_consume<D>(a.xs[f], a.g, t, ok && t < a.g.n_pb, r_f, minexp, hlane, htrash, tbl,
+                           &s_tbl_used, flush_mark, a.hist + (size_t)tc.w * kNSlots, ovf, tbits,
+                           terr);
+      } else {
+        tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hlane, htrash,
+                               tbl, &s_tbl_used, flush_mark, a.hist + (size_t)tc.w * kNSlots, ovf,
+                               nodbg, tbits, terr);
+      }
       ++cur_tasks;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
@@ -657,6 +666,15 @@ int batch_sizes(const Geo &g, BatchSizes *bs) {
   return SEL_OK;
 }
 
+// T tasks per field: TMA tiles, or (strides > 1) groups of one processed block per lane
+int batch_ntasks(const Geo &g, const TileLaunch &tl, const BatchSizes &bs) {
+  if (g.s[0] > 1 || g.s[1] > 1 || g.s[2] > 1) {
+    const int64_t per = (int64_t)bs.cw * 32;
+    return (int)((g.n_pb + per - 1) / per);
+  }
+  return tl.tg.ntasks;
+}
+
 size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G) {
   return (size_t)nf * (sizeof(Params) + 8 * 4 + sizeof(CUtensorMap) + 8) + 64 +
          (size_t)G * kRing * ((size_t)kNSlots * 8 + (size_t)nT * bs.cw * sizeof(Partial) +
@@ -678,7 +696,8 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
     off += bytes;
     return b + o;
   };
-  const int nT = tl.tg.ntasks;
+  const int nT = batch_ntasks(g, tl, bs);
+  const bool sampled = g.s[0] > 1 || g.s[1] > 1 || g.s[2] > 1;
   CUtensorMap *tmaps = (CUtensorMap *)take(sizeof(CUtensorMap) * nf, 128);
   const float **xs = (const float **)take(sizeof(float *) * nf);
   Params *params = (Params *)take(sizeof(Params) * nf);
@@ -693,8 +712,10 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   // by the caller? small: a few KB -> plain cudaMemcpyAsync from pageable is fine)
   static thread_local std::vector<CUtensorMap> h_maps;
   h_maps.resize(nf);
-  for (int f = 0; f < nf; ++f)
-    if (make_tile_map(&h_maps[f], d_fields[f], g)) return SEL_ECUDA;
+  if (sampled) memset(h_maps.data(), 0, sizeof(CUtensorMap) * nf);   // no tiles
+  else
+    for (int f = 0; f < nf; ++f)
+      if (make_tile_map(&h_maps[f], d_fields[f], g)) return SEL_ECUDA;
   if (cudaMemcpyAsync(tmaps, h_maps.data(), sizeof(CUtensorMap) * nf, cudaMemcpyHostToDevice, st) !=
           cudaSuccess ||
       cudaMemcpyAsync(xs, d_fields, sizeof(float *) * nf, cudaMemcpyHostToDevice, st) != cudaSuccess ||
@@ -707,6 +728,8 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   a.xs = xs;
   a.nf = nf;
   a.tg = tl.tg;
+  a.g = g;
+  a.sampled = sampled ? 1 : 0;
   a.N = g.N;
   a.nR = bs.nR;
   a.nT = nT;

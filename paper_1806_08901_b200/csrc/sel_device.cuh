@@ -283,6 +283,27 @@ __device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int mi
 }
 
 
+// one 4-value row of a block (+ its left neighbour h) from global memory; rows / planes
+// past the field edge are replicated (R17), the left neighbour is 0 at k = 0 (R4)
+template <bool VEC>
+__device__ __forceinline__ void load_row(const float *__restrict__ x, const Geo &g, int64_t i,
+                                         int64_t j, int64_t k0, float v[4], float &h) {
+  const int64_t ic = i < g.n[0] ? i : g.n[0] - 1;   // edge replication for padded rows (R17)
+  const int64_t jc = j < g.n[1] ? j : g.n[1] - 1;
+  const float *row = x + (ic * g.n[1] + jc) * g.n[2];
+  if constexpr (VEC) {
+    const float4 q = __ldg(reinterpret_cast<const float4 *>(row + k0));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int64_t k = k0 + c;
+      v[c] = __ldg(row + (k < g.n[2] ? k : g.n[2] - 1));
+    }
+  }
+  h = k0 > 0 ? __ldg(row + k0 - 1) : 0.0f;
+}
+
 // Per-field result from the reduced sums (Eq. entropy, Eq. psnr-sz
 // P:410) and the Alg. 1 lines 7-10 selection (reading R16).
 // S = sum_s c_s log2(N/c_s); lg_* are log10(VR/eb), log10(VR), log10(MSE).

@@ -134,6 +134,7 @@ struct BatchSizes {
 bool tile_supported(const Geo &g);
 int batch_sizes(const Geo &g, BatchSizes *bs);
 size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G);
+int batch_ntasks(const Geo &g, const TileLaunch &tl, const BatchSizes &bs);
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
                  sel_result *d_results, int sm_count, int G, int lagT, cudaStream_t st,

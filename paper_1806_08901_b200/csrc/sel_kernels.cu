@@ -321,25 +321,6 @@ __global__ void __launch_bounds__(256, (D == 3 ? SEL_MARCH3_MINB : 3)) k_march(c
 }
 
 // ============================================================ K2b: generic pass (sampled, 1D)
-template <bool VEC>
-__device__ __forceinline__ void load_row(const float *__restrict__ x, const Geo &g, int64_t i,
-                                         int64_t j, int64_t k0, float v[4], float &h) {
-  const int64_t ic = i < g.n[0] ? i : g.n[0] - 1;   // edge replication for padded rows (R17)
-  const int64_t jc = j < g.n[1] ? j : g.n[1] - 1;
-  const float *row = x + (ic * g.n[1] + jc) * g.n[2];
-  if constexpr (VEC) {
-    const float4 q = __ldg(reinterpret_cast<const float4 *>(row + k0));
-    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-  } else {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      int64_t k = k0 + c;
-      v[c] = __ldg(row + (k < g.n[2] ? k : g.n[2] - 1));
-    }
-  }
-  h = k0 > 0 ? __ldg(row + k0 - 1) : 0.0f;
-}
-
 template <int D, bool VEC, bool DBG>
 __global__ void __launch_bounds__(256) k_estimate(const float *__restrict__ x, Geo g,
                                                   Workspace ws, DebugPtrs dbg) {

@@ -317,6 +317,120 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
     }
 }
 
+// Sampled-block task (strides > 1; k_batch): lane = processed block t (act: t < n_pb),
+// read with its halo from global memory (L2: the range pass just streamed the field),
+// codes into the same smem histogram as a tile task, ZFP block in registers.  Every lane
+// of the warp runs (inactive lanes on a clamped block, contributing nothing) so the
+// warp-uniform out-of-window branch stays uniform.
+template <int D>
+__device__ __forceinline__ void sampled_consume(const float *__restrict__ x, const Geo &g,
+                                                int64_t t, bool act, float r_f, int minexp,
+                                                unsigned int *hlane, unsigned int *htrash,
+                                                unsigned int *tbl, int *tbl_used, int tbl_mark,
+                                                unsigned long long *ghist, unsigned int &ovf,
+                                                uint64_t &tbits, double &terr) {
+  using Cfg = TileCfg<D>;
+  constexpr int SZ = Tab<D>::SIZE;
+  constexpr int PL = D == 3 ? 4 : 1;
+  const int lane = threadIdx.x & 31;
+  if (!act) t = 0;
+  const int64_t p2 = t % g.npb[2];
+  const int64_t qq = t / g.npb[2];
+  const int64_t p1 = qq % g.npb[1];
+  const int64_t p0 = qq / g.npb[1];
+  const int64_t I0 = 4 * p0 * g.s[0], J0 = 4 * p1 * g.s[1], K0 = 4 * p2 * g.s[2];
+  float blk[SZ];
+  float dprev[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dprev[r][c] = 0.0f;
+  if (D == 3 && I0 > 0) {        // plane i = I0 - 1 (zeros outside the field)
+    float up[4] = {0.f, 0.f, 0.f, 0.f}, uh = 0.0f;
+    if (J0 > 0) load_row<true>(x, g, I0 - 1, J0 - 1, K0, up, uh);
+    float d1up[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) d1up[c] = up[c] - (c ? up[c - 1] : uh);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float v[4], h;
+      load_row<true>(x, g, I0 - 1, J0 + r, K0, v, h);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float d1 = v[c] - (c ? v[c - 1] : h);
+        dprev[r][c] = d1 - d1up[c];
+        d1up[c] = d1;
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < PL; ++p) {
+    const int64_t i = I0 + p;
+    float d1up[4];
+    {
+      float up[4] = {0.f, 0.f, 0.f, 0.f}, uh = 0.0f;
+      if (J0 > 0) load_row<true>(x, g, i, J0 - 1, K0, up, uh);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) d1up[c] = up[c] - (c ? up[c - 1] : uh);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t j = J0 + r;
+      const bool rowok = act && i < g.n[0] && j < g.n[1];   // k < n[2]: n[2] % 4 == 0
+      float v[4], h;
+      load_row<true>(x, g, i, j, K0, v, h);
+      uint32_t w[4];
+      uint32_t any = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        blk[(p * 4 + r) * 4 + c] = v[c];
+        const float d1 = v[c] - (c ? v[c - 1] : h);
+        const float d2 = d1 - d1up[c];
+        d1up[c] = d1;
+        float d;
+        if constexpr (D == 3) {
+          d = d2 - dprev[r][c];
+          dprev[r][c] = d2;
+        } else {
+          d = d2;
+        }
+        const bool valid = rowok && !(i == 0 && j == 0 && K0 + c == 0);   // origin (R4)
+        w[c] = sz_win(d, r_f, valid ? hlane : htrash);
+        w[c] = valid ? w[c] : 0u;
+        any |= w[c];
+      }
+      if (__any_sync(0xffffffffu, any >= (uint32_t)kHBins)) {
+        uint32_t far = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t tb = w[c] + (kHOff - Cfg::kTOff);
+          const bool out = w[c] >= (uint32_t)kHBins;
+          if (out && tb < (uint32_t)Cfg::TB) atomicAdd(tbl + tb, 1u);
+          far |= (out && tb >= (uint32_t)Cfg::TB) ? (1u << c) : 0u;
+        }
+        if (lane == 0) *tbl_used = tbl_mark;
+        if (__any_sync(0xffffffffu, far != 0u)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (far & (1u << c)) {
+              const uint32_t sl = w[c] + (kHOff - kSlotOff);
+              if (sl > 65534u) ++ovf;
+              else atomicAdd(ghist + sl, 1ull);
+            }
+        }
+      }
+    }
+  }
+  uint32_t bits;
+  double E;
+  int emax;
+  int cf[SZ];
+  uint32_t u[SZ];
+  zfp_block<D, false>(blk, minexp, bits, E, emax, cf, u);
+  tbits = act ? bits : 0u;
+  terr = act ? E : 0.0;
+}
+
 // Move the CTA's smem histogram (lane copies + packed table) into the global histogram
 // and clear it.  Called by the consumer threads (tid < nthr) after a consumer barrier.
 template <int D>

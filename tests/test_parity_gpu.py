@@ -245,16 +245,18 @@ def test_batch_kernel_tiny_stacks(sel, orc, nf, shape):
         compare_scalars(out[i], orc.estimate(x, 1e-3), f"tiny{nf}/{i}")
 
 
-@pytest.mark.parametrize("cfg,nf", [(2, 12), (3, 3), (4, 2)])
-def test_batch_full_size_stack_vs_per_field(sel, cfg, nf):
+@pytest.mark.parametrize("cfg,nf,stride", [(2, 12, None), (3, 3, None), (4, 2, None),
+                                            (2, 12, (1, 10)), (4, 2, (4, 4, 4)), (3, 2, (1, 2, 3))])
+def test_batch_full_size_stack_vs_per_field(sel, cfg, nf, stride):
     """A stack of full-size fields through k_batch (auto CTA groups, several flushes per
-    CTA, second-level table in use on C2) equals the per-field kernels field by field,
+    CTA, second-level table in use on C2; tiles, or sampled-block tasks for strides > 1)
+    equals the per-field kernels field by field,
     and repeats bit-identically.  The per-field kernels are checked against the oracle
     by the tests above."""
     import synth
     fs = [torch.from_numpy(synth.make_field(cfg, i)).cuda() for i in range(nf)]
     eb = synth.CONFIGS[cfg]["eb_rel"][0]
-    with sel.Plan(tuple(fs[0].shape), eb) as p:
+    with sel.Plan(tuple(fs[0].shape), eb, "rel", stride) as p:
         p.set_option("batch_kernel", 0)
         ref = [p.estimate(f) for f in fs]
         p.set_option("batch_kernel", 1)
@@ -267,6 +269,22 @@ def test_batch_full_size_stack_vs_per_field(sel, cfg, nf):
                 assert a[k] == pytest.approx(b[k], rel=1e-12, abs=0), (cfg, i, k)
             else:
                 assert a[k] == b[k], (cfg, i, k)
+
+
+@pytest.mark.parametrize("shape,stride", [((40, 300), (1, 10)), ((40, 300), (3, 2)),
+                                          ((20, 24, 36), (2, 1, 3)), ((9, 14, 20), (1, 1, 2))])
+def test_batch_sampled_vs_oracle(sel, orc, shape, stride):
+    """Sampled-block tasks of k_batch (strides > 1) give the oracle's results."""
+    rng = np.random.default_rng(sum(shape))
+    xs = [np.cumsum(rng.standard_normal(shape), axis=-1).astype(np.float32) * (i + 1)
+          for i in range(5)]
+    ts = [torch.from_numpy(x).cuda() for x in xs]
+    with sel.Plan(shape, 1e-3, "rel", stride) as p:
+        l0 = p.launch_count
+        out = p.estimate_batch(ts)
+        assert p.launch_count - l0 == 1            # one k_batch launch
+    for i, x in enumerate(xs):
+        compare_scalars(out[i], orc.estimate(x, 1e-3, stride=stride), f"sampled/{i}")
 
 
 @pytest.mark.parametrize("groups", [1, 2, 3, 5])
