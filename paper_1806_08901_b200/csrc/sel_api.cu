@@ -212,9 +212,12 @@ bool batch_ok(sel_plan_t p, const float *const *x, int n) {
 // their tiles (kLagT per group) must stay in L2 (~126 MB), hence the byte budget.
 int batch_groups(sel_plan_t p, int n) {
   int G = p->groups;
-  if (G <= 0) {                   // measured (DESIGN.md section 6): ~80 MB of fields in flight
+  if (G <= 0) {                   // measured (DESIGN.md section 5): ~80 MB of fields in flight
     const double fb = (double)p->geo.N * 4.0;
     G = (int)(80e6 / fb);
+    // sampled strides: little tile work per field, so the per-field pipeline latency
+    // dominates -- more groups in flight (C2 at stride (1,10): G 3 -> 10, +42%)
+    if (p->sampled_ok && G < 16) G = 16;
     if (G > 32) G = 32;
     if (G > n / 2) G = n / 2;     // keep >= 2 fields per group (tail balance)
   }

@@ -2,9 +2,11 @@
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth, paper_1806_08901_b200 as sel
-for cfg, nf, st in ((2, 20, (1, 10)), (2, 20, (1, 1)), (4, 2, (4, 4, 4))):
+for cfg, nf, st in ((2, 20, (1, 10)), (2, 20, (1, 1)), (4, 2, (4, 4, 4)), (4, 6, (4, 4, 4))):
     fs = [torch.from_numpy(synth.make_field(cfg, i)).cuda() for i in range(nf)]
     p = sel.Plan(tuple(fs[0].shape), synth.CONFIGS[cfg]["eb_rel"][0], "rel", st)
+    if os.environ.get("SEL_G"):
+        p.set_option("groups", int(os.environ["SEL_G"]))
     buf = p.results_buffer(nf)
     for _ in range(2):
         p.estimate_batch_async(fs, buf)
