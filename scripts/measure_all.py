@@ -1,0 +1,60 @@
+"""Throughput of k_batch on every BASELINE config (developer tool; writes a markdown table).
+
+    python scripts/measure_all.py > gpurun_out/throughput.md
+Fields already in HBM, steps = one sel_estimate_batch_async of the whole stack + D2H of
+the results, CUDA events, 2 warm-up + 5 timed steps; GB/s = float32 input bytes / time.
+"""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, synth, paper_1806_08901_b200 as sel
+
+PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")))["hbm_gbs"]
+
+
+def run(fields, eb, stride, label):
+    shape = tuple(fields[0].shape)
+    p = sel.Plan(shape, eb, "rel", stride)
+    buf = p.results_buffer(len(fields))
+    for _ in range(2):
+        p.estimate_batch_async(fields, buf)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        p.estimate_batch_async(fields, buf)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    res = p.decode_results(buf, len(fields))
+    nsz = sum(1 for r in res if r["choice"] == 0)
+    gbs = len(fields) * fields[0].numel() * 4 / ms / 1e6
+    print(f"| {label} | {len(fields)} | {eb:g} | {stride or 'all'} | {ms / len(fields) * 1e3:.1f} | "
+          f"{gbs:.0f} | {100 * gbs / PEAK:.1f} | {nsz} / {len(fields) - nsz} |", flush=True)
+    p.close()
+
+
+print(f"| workload | fields | eb_rel | stride | us / field | GB/s | % of HBM ({PEAK:g} GB/s) | SZ / ZFP chosen |")
+print("|---|---:|---:|---|---:|---:|---:|---|")
+f1 = [torch.from_numpy(synth.c1_field(seed=i)).cuda() for i in range(256)]
+run(f1, 1e-4, None, "C1 256x256 (x256 seeds)")
+del f1
+f2 = [torch.from_numpy(synth.make_field(2, i)).cuda() for i in range(100)]
+run(f2, 1e-4, None, "C2 1800x3600")
+run(f2, 1e-4, (1, 10), "C2 1800x3600")
+del f2
+f3 = [torch.from_numpy(synth.make_field(3, i)).cuda() for i in range(13)]
+for eb in (1e-3, 1e-4, 1e-5):
+    run(f3, eb, None, "C3 100x500x500")
+del f3
+f4 = [torch.from_numpy(synth.make_field(4, i)).cuda() for i in range(6)]
+run(f4, 1e-4, None, "C4 512^3")
+run(f4, 1e-4, (4, 4, 4), "C4 512^3")
+del f4
+torch.cuda.empty_cache()
+for mix in (0, 1, 2):
+    t0 = time.time()
+    x = torch.from_numpy(synth.make_field(5, mix)).cuda()
+    for eb in (1e-2, 1e-4, 1e-6):
+        run([x], eb, None, f"C5 1024^3 w={(0, 0.5, 1)[mix]}")
+    del x
+    torch.cuda.empty_cache()
