@@ -95,9 +95,19 @@ typedef struct {
 int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double eb,
              const int32_t *stride, int32_t block);
 
-/* Options: "sz_offset_bits" (default 0.5); "debug" (1 = dump intermediates
- * for sel_debug_copy; test sizes only); "kernel_timing" (1 = record CUDA events
- * around every launch, read with sel_kernel_times). Errors: SEL_EINVAL. */
+/* Options:
+ *   "sz_offset_bits"  SZ bit-rate offset beta (default 0.5)
+ *   "debug"           1 = dump intermediates for sel_debug_copy (per-field kernels;
+ *                     test sizes only)
+ *   "kernel_timing"   1 = record CUDA events around every launch (sel_kernel_times)
+ *   "batch_kernel"    1 (default) = one persistent k_batch launch per call where the
+ *                     shape allows (2D/3D, fastest extent % 4 == 0, 16-byte aligned
+ *                     fields); 0 = per-field kernels
+ *   "pipeline"        1 (default) = per-field kernels of a batch on three streams
+ *   "groups"          k_batch CTA groups, 0 (default) = automatic, else 1..148
+ *   "lag"             k_batch phases between a field's range pass and its tiles, 1..4
+ *                     (default 2)
+ * None changes any result (tests).  Errors: SEL_EINVAL (unknown key, value out of range). */
 int sel_set_option(sel_plan_t plan, const char *key, double value);
 
 /* Estimate one field already in device memory (d_field: device, N floats).
