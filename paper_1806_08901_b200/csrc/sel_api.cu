@@ -202,6 +202,7 @@ int enqueue_est(sel_plan_t p, const float *x, int f, cudaStream_t st, TimingSlot
 // finalize of every field as one task stream; results land in d_res[0..n).
 bool batch_ok(sel_plan_t p, const float *const *x, int n) {
   if (!(p->tile_ok || p->sampled_ok) || !p->use_batch || p->debug) return false;
+  if (p->geo.N >= (int64_t)1 << 32) return false;   // k_batch histograms are u32
   for (int f = 0; f < n; ++f)
     if (((uintptr_t)x[f] & 15u) != 0) return false;
   return true;

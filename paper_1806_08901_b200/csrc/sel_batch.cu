@@ -27,7 +27,13 @@ namespace sel {
 constexpr int kFinTasks = 8;                   // F tasks per field (8192 slots each)
 constexpr int kRing = 3;                       // histogram / partial buffers (field % 3)
 // phase p: R(p), T(p - lagT), F(p - lagF) with lagF = lagT + 2 (BatchArgs; default 2 / 4)
-constexpr int kRWarps = 2;                     // consumer warps reducing one range chunk
+// Global histograms are u32 (a field has < 2^32 values: batch_ok) with slot s at word
+// 1 + s of its ring slot, so the smem window / table land on 16-byte aligned global
+// addresses for cp.reduce.async.bulk; stride 65,540 words keeps every ring slot aligned.
+constexpr int kH32Stride = kNSlots + 4;
+#ifndef SEL_RWARPS
+#define SEL_RWARPS 64                          // range chunk split over min(this, CW) warps
+#endif
 #ifndef SEL_BATCH_PROF
 #define SEL_BATCH_PROF 0                       // 1: per-CTA cycle counters (sel_dev_batch_profile)
 #endif
@@ -73,7 +79,7 @@ struct BatchArgs {
   unsigned int *fin_ready;        // [nf]
   int lagT, lagF;                 // phases from a field's range pass to its tiles / finalize
   int G;                          // CTA groups: group g = blockIdx % G runs fields f = g (mod G)
-  unsigned long long *hist;       // [G * kRing][kNSlots], slot ring(f)
+  unsigned int *hist;             // [G * kRing][kH32Stride] (slot s at 1 + s), slot ring(f)
   Partial *tpart;                 // [G * kRing][nT * CW]
   FPart *fpart;                   // [G * kRing][kFinTasks]
   unsigned int *task_ctr;         // [G]
@@ -182,6 +188,19 @@ __device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *m
       : "memory");
 }
 
+// Bulk reduction shared -> global by the TMA engine (the histogram flush): one instruction
+// adds a whole smem array into global memory at L2, instead of one atomic per bin.
+__device__ __forceinline__ void bulk_reduce_add_u32(unsigned int *gdst, const void *ssrc, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u32 [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ float fmin_nan(float a, float b) {   // NaN if either is NaN
   float r;
@@ -226,13 +245,13 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   using Cfg = TileCfg<D>;
   constexpr int CW = Cfg::CW;
   constexpr int NC = CW * 32;                  // consumer threads
+  constexpr int kRWarps = SEL_RWARPS > CW ? CW : SEL_RWARPS;   // consumer warps reducing one range chunk
   extern __shared__ float smem_dyn[];
   float *const base = smem_dyn + (((128u - (smem_u32(smem_dyn) & 127u)) & 127u) >> 2);
   unsigned int *const hist = reinterpret_cast<unsigned int *>(base + Cfg::STAGES * Cfg::STAGE_FLOATS);
-  unsigned int *const tbl = hist + Cfg::HIST_WORDS;
   // barriers + per-stage descriptors, 16-byte aligned (hist starts 128-byte aligned)
   uint64_t *const full_bar =
-      reinterpret_cast<uint64_t *>(hist + ((Cfg::HIST_WORDS + Cfg::TBL_WORDS + 3) & ~3));
+      reinterpret_cast<uint64_t *>(hist + Cfg::HIST_WORDS);
   uint64_t *const empty_bar = full_bar + Cfg::STAGES;
   // per stage, decoded once by the producer: {kind | end flag, f, id, phase} and the tile
   // coordinates {btk, btj, bi}
@@ -240,7 +259,8 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   int4 *const stage_tile = stage_desc + Cfg::STAGES;
   __shared__ double s_red[3][CW];
   __shared__ unsigned long long s_redu[2][CW];
-  __shared__ int s_tbl_used;
+  constexpr int NCHUNK = Cfg::W / kChunk;
+  __shared__ int s_chunk[NCHUNK];                // window chunks with a nonzero bin (flush)
   __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2];
   __shared__ RelReq s_q[kRelQ];
   __shared__ unsigned int s_qhead, s_qtail;
@@ -250,7 +270,6 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   const int nfl = (a.nf - grp + a.G - 1) / a.G;                  // this group's fields
   const long long ntot = (long long)nfl * (a.nR + a.nT + kFinTasks);
   if (tid == 0) {
-    s_tbl_used = 0;
     s_qhead = 0u;
     s_qtail = 0u;
     for (int k = 0; k < 2; ++k) {
@@ -262,7 +281,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     }
     fence_barrier_init();
   }
-  for (int i = tid; i < Cfg::HIST_WORDS + Cfg::TBL_WORDS; i += (int)blockDim.x) hist[i] = 0u;
+  for (int i = tid; i < Cfg::HIST_WORDS; i += (int)blockDim.x) hist[i] = 0u;
   __syncthreads();
 
   // ------------------------------------------------------------------ producer
@@ -314,7 +333,11 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         stage_desc[stage] = make_int4(t0.kind, t0.f, t0.id, t0.phase);
         stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, t0.slot);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
-        if (t0.kind == KIND_T && !a.sampled) {
+        if (Cfg::DIRECT && t0.kind == KIND_T) {
+          // direct tiles: no staged data, the consumers read the box from L2 (prefetched
+          // when the task was claimed)
+          mbar_arrive(&full_bar[stage]);
+        } else if (t0.kind == KIND_T && !a.sampled) {
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
             tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
@@ -380,11 +403,8 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   }
 
   // ------------------------------------------------------------------ consumers
-  unsigned int *const hlane = hist + (lane % Cfg::COPIES) * kHStride;
-  unsigned int *const htrash = hist + Cfg::COPIES * kHStride;
   int cur = -1;                    // field owning the smem histogram
   int cur_slot = 0;                // its ring slot
-  int flush_mark = 1;              // flush interval number (s_tbl_used starts at 0)
   unsigned int cur_tasks = 0;      // its T tasks since the last flush
   unsigned int ovf = 0;
   bool ok = false;
@@ -409,18 +429,61 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     PROF(pc[5] += clock64() - tp0);
   };
 
-  auto flush = [&]() {             // all consumers, same task: move smem histogram to global
-    unsigned long long *gh = a.hist + (size_t)cur_slot * kNSlots;
+  // Histogram flush (all consumers, same task): the warps mark the window's nonzero
+  // 1024-bin chunks, tid 0 adds those chunks into the field's global histogram with bulk
+  // reductions (the TMA engine, cp.reduce.async.bulk .add.u32), the consumers clear them
+  // once they have been read, and the publication (tdone) waits for the reductions to
+  // complete.
+  auto flush = [&]() {
+    unsigned int *gh = a.hist + (size_t)cur_slot * kH32Stride + 1;
     const long long q0 = PCLOCK();
-    ovf_flush(ovf, gh);
+    {
+      unsigned int o = ovf;
+#pragma unroll
+      for (int k = 16; k > 0; k >>= 1) o += __shfl_xor_sync(0xffffffffu, o, k);
+      if (lane == 0 && o) atomicAdd(gh + kOvfSlot, o);
+    }
     ovf = 0;
     const long long q1 = PCLOCK();
     consumer_sync<NC>();
     const long long q2 = PCLOCK();
     PROF(pc[6] += 1);
-    tile_hist_flush<D>(hist, tbl, &s_tbl_used, flush_mark, gh, tid, NC);
+    for (int c = warp; c < NCHUNK; c += CW) {
+      const uint4 *h4 = reinterpret_cast<const uint4 *>(hist + c * kChunk);
+      uint32_t any = 0u;
+#pragma unroll
+      for (int k = 0; k < kChunk / 128; ++k) {
+        const uint4 v = h4[k * 32 + lane];
+        any |= v.x | v.y | v.z | v.w;
+      }
+      any = __any_sync(0xffffffffu, any != 0u);
+      if (lane == 0) s_chunk[c] = (int)any;
+    }
+    consumer_sync<NC>();
+    if (tid == 0) {
+      fence_proxy_async_global();
+      int n = 0;
+      for (int c = 0; c < NCHUNK; ++c)
+        if (s_chunk[c]) {
+          bulk_reduce_add_u32(gh + (kCenter - Cfg::W / 2) + c * kChunk, hist + c * kChunk, kChunk * 4);
+          ++n;
+        }
+      bulk_commit();
+      if (n) bulk_wait_read();
+    }
+    consumer_sync<NC>();
+    for (int c = warp; c < NCHUNK; c += CW)
+      if (s_chunk[c]) {
+        uint4 *h4 = reinterpret_cast<uint4 *>(hist + c * kChunk);
+#pragma unroll
+        for (int k = 0; k < kChunk / 128; ++k) h4[k * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
+      }
     const long long q3 = PCLOCK();
-    consumer_sync<NC>();           // every consumer's atomics issued before the release
+    consumer_sync<NC>();           // cleared before anyone counts again
+    if (tid == 0) {                // the reductions are complete before tdone publishes them
+      bulk_wait_all();
+      fence_proxy_async_global();
+    }
     const long long q4 = PCLOCK();
     if (SEL_BATCH_PROF && a.prof && tid == 0) {
       atomicAdd(a.prof + 148 * 8 + 0, (unsigned long long)(q1 - q0));
@@ -428,7 +491,6 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       atomicAdd(a.prof + 148 * 8 + 2, (unsigned long long)(q3 - q2));
       atomicAdd(a.prof + 148 * 8 + 3, (unsigned long long)(q4 - q3));
     }
-    ++flush_mark;                  // codes from now on mark the table with the next interval
     if (tid == 0) enqueue(REQ_T, cur, cur_tasks, 0u, 0u, 0u);
     cur = -1;
     cur_tasks = 0;
@@ -490,6 +552,10 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
 
     if (kind == KIND_T) {
       const int4 tc = stage_tile[stage];
+      if constexpr (Cfg::DIRECT) {   // descriptor read: the slot is free again
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      }
       if (cur < 0) {               // first tile of field f here: params, ring slot free
         // per warp (no CTA barrier): lane 0 acquires the flags, the warp barrier orders
         // the lanes' L2 reads (ld.cg: never a stale L1 line) after it
@@ -508,17 +574,22 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       double terr = 0.0;
       if (a.sampled) {             // processed blocks id*NC .. +NC-1, one per consumer lane
         const int64_t t = ((int64_t)id * CW + warp) * 32 + lane;
-        sampled_consume<D>(a.xs[f], a.g, t, ok && t < a.g.n_pb, r_f, minexp, hlane, htrash, tbl,
-                           &s_tbl_used, flush_mark, a.hist + (size_t)tc.w * kNSlots, ovf, tbits,
+        sampled_consume<D>(a.xs[f], a.g, t, ok && t < a.g.n_pb, r_f, minexp, hist,
+                           a.hist + (size_t)tc.w * kH32Stride + 1, ovf, tbits,
                            terr);
+      } else if constexpr (Cfg::DIRECT) {
+        tile_consume_direct<false>(a.xs[f], tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hist,
+                                   a.hist + (size_t)tc.w * kH32Stride + 1, ovf, nodbg, tbits, terr);
       } else {
-        tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hlane, htrash,
-                               tbl, &s_tbl_used, flush_mark, a.hist + (size_t)tc.w * kNSlots, ovf,
+        tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hist,
+                               a.hist + (size_t)tc.w * kH32Stride + 1, ovf,
                                nodbg, tbits, terr);
       }
       ++cur_tasks;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      if constexpr (!Cfg::DIRECT) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      }
       task_store(a.tpart + (size_t)tc.w * a.nT * CW, id * CW + warp, tbits, terr);
     } else if (kind == KIND_R) {
       // ---- min / max / non-finite of the staged chunk (R1) by kRWarps consumer warps
@@ -531,12 +602,13 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       } else {
         const long long lo = (long long)id * a.rchunk;
         const int n4 = (int)min((long long)a.rchunk, a.N - lo) / 4;
+        const float4 *src = reinterpret_cast<const float4 *>(S);
         // min propagates NaN (min.NaN), so non-finite values show up in the reduced
         // min / max themselves: NaN -> mn is NaN, +-inf -> mx / mn infinite
         float mn = INFINITY, mx = -INFINITY;
-#pragma unroll 4
+#pragma unroll 8
         for (int i = slot * 32 + lane; i < n4; i += kRWarps * 32) {
-          const float4 q = reinterpret_cast<const float4 *>(S)[i];
+          const float4 q = src[i];
           mn = fmin_nan(mn, fmin_nan(fmin_nan(q.x, q.y), fmin_nan(q.z, q.w)));
           mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
         }
@@ -565,7 +637,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
       if (tid == 0) spin_until(a.tdone + f, (unsigned)a.nT);
       consumer_sync<NC>();
-      unsigned long long *gh = a.hist + (size_t)slot * kNSlots;
+      unsigned int *gh = a.hist + (size_t)slot * kH32Stride + 1;
       const Partial *tpf = a.tpart + (size_t)slot * a.nT * CW;
       FPart *fpf = a.fpart + (size_t)slot * kFinTasks;
       // ---- 1/8 of the histogram: sum c log2(N/c), re-zero; and 1/8 of the tile partials
@@ -575,11 +647,11 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       double acc = 0.0;
       unsigned long long novf = 0;
       for (int s = id * PER + tid; s < (id + 1) * PER; s += NC) {
-        const unsigned long long c = __ldcg(gh + s);
+        const unsigned int c = __ldcg(gh + s);
         if (c) {
           const double cd = (double)c;
           acc += cd * (lN - log2(cd));
-          gh[s] = 0ull;
+          gh[s] = 0u;
         }
         if (s == kOvfSlot) novf = c;
       }
@@ -655,6 +727,7 @@ const void *batch_fn() { return (const void *)k_batch<D>; }
 
 int batch_sizes(const Geo &g, BatchSizes *bs) {
   const int d3 = g.ndims == 3;
+  // range chunk: one smem stage
   bs->rchunk = d3 ? (TileCfg<3>::STAGE_FLOATS & ~3) : (TileCfg<2>::STAGE_FLOATS & ~3);
   bs->nR = (int)((g.N + bs->rchunk - 1) / bs->rchunk);
   bs->smem = d3 ? TileCfg<3>::SMEM : TileCfg<2>::SMEM;
@@ -677,7 +750,7 @@ int batch_ntasks(const Geo &g, const TileLaunch &tl, const BatchSizes &bs) {
 
 size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G) {
   return (size_t)nf * (sizeof(Params) + 8 * 4 + sizeof(CUtensorMap) + 8) + 64 +
-         (size_t)G * kRing * ((size_t)kNSlots * 8 + (size_t)nT * bs.cw * sizeof(Partial) +
+         (size_t)G * kRing * ((size_t)kH32Stride * 4 + (size_t)nT * bs.cw * sizeof(Partial) +
                               kFinTasks * sizeof(FPart)) +
          8192;
 }
@@ -704,7 +777,7 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   const size_t nctr = 8 * (size_t)nf + (size_t)G;
   unsigned int *ctrs = (unsigned int *)take(sizeof(unsigned int) * nctr);
   const size_t nslot = (size_t)G * kRing;
-  unsigned long long *hst = (unsigned long long *)take((size_t)kNSlots * 8 * nslot);
+  unsigned int *hst = (unsigned int *)take((size_t)kH32Stride * 4 * nslot);
   Partial *tp = (Partial *)take(sizeof(Partial) * (size_t)nT * bs.cw * nslot);
   FPart *fp = (FPart *)take(sizeof(FPart) * kFinTasks * nslot);
   if (off > state_bytes) return SEL_EINVAL;
@@ -721,7 +794,7 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
       cudaMemcpyAsync(xs, d_fields, sizeof(float *) * nf, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemsetAsync(ctrs, 0, sizeof(unsigned int) * nctr, st) != cudaSuccess ||
       cudaMemsetAsync(ctrs + 6 * (size_t)nf, 0xff, sizeof(unsigned int) * nf, st) != cudaSuccess ||
-      cudaMemsetAsync(hst, 0, (size_t)kNSlots * 8 * nslot, st) != cudaSuccess)
+      cudaMemsetAsync(hst, 0, (size_t)kH32Stride * 4 * nslot, st) != cudaSuccess)
     return SEL_ECUDA;
   BatchArgs a;
   a.tmaps = tmaps;

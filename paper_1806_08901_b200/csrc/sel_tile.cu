@@ -21,31 +21,29 @@ namespace sel {
 
 template <int D, bool DBG>
 __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
-    k_tile(const __grid_constant__ CUtensorMap tmap, TileGeo tg, Workspace ws, DebugPtrs dbg) {
+    k_tile(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ x, TileGeo tg,
+           Workspace ws, DebugPtrs dbg) {
   using Cfg = TileCfg<D>;
   constexpr int CW = Cfg::CW;
   extern __shared__ float smem_dyn[];
   // 128-byte align the stage ring (TMA destination) without leaving the shared window
   float *const base = smem_dyn + (((128u - (smem_u32(smem_dyn) & 127u)) & 127u) >> 2);
   unsigned int *const hist = reinterpret_cast<unsigned int *>(base + Cfg::STAGES * Cfg::STAGE_FLOATS);
-  unsigned int *const tbl = hist + Cfg::HIST_WORDS;
   // barriers + per-stage descriptors, 16-byte aligned (hist starts 128-byte aligned)
   uint64_t *const full_bar =
-      reinterpret_cast<uint64_t *>(hist + ((Cfg::HIST_WORDS + Cfg::TBL_WORDS + 3) & ~3));
+      reinterpret_cast<uint64_t *>(hist + Cfg::HIST_WORDS);
   uint64_t *const empty_bar = full_bar + Cfg::STAGES;
   int4 *const stage_task = reinterpret_cast<int4 *>(empty_bar + Cfg::STAGES);   // {t, btk, btj, bi}
 
-  __shared__ int s_tbl_used;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    s_tbl_used = 0;
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], CW);
     }
     fence_barrier_init();
   }
-  for (int i = threadIdx.x; i < Cfg::HIST_WORDS + Cfg::TBL_WORDS; i += Cfg::THREADS) hist[i] = 0u;
+  for (int i = threadIdx.x; i < Cfg::HIST_WORDS; i += Cfg::THREADS) hist[i] = 0u;
   __syncthreads();
   grid_dep_wait();   // k_minmax done: params valid, the task counter was reset by the
                      // previous field's finalize (which k_minmax waited for)
@@ -72,11 +70,19 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
         const int bi = rest / tg.ntj;
         stage_task[stage] = make_int4(t, btk, btj, bi);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
-        mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-        if constexpr (D == 3)
-          tma_load_3d(dst, &tmap, 128 * btk - 4, 4 * CW * btj - 1, 4 * bi - 1, &full_bar[stage]);
-        else
-          tma_load_2d(dst, &tmap, 128 * btk - 4, 4 * CW * btj - 1, &full_bar[stage]);
+        if constexpr (Cfg::DIRECT) {     // descriptor only; the tile box goes to L2
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                           reinterpret_cast<uint64_t>(&tmap)),
+                       "r"(128 * btk - 4), "r"(4 * CW * btj - 1), "r"(4 * bi - 1)
+                       : "memory");
+          mbar_arrive(&full_bar[stage]);
+        } else {
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          if constexpr (D == 3)
+            tma_load_3d(dst, &tmap, 128 * btk - 4, 4 * CW * btj - 1, 4 * bi - 1, &full_bar[stage]);
+          else
+            tma_load_2d(dst, &tmap, 128 * btk - 4, 4 * CW * btj - 1, &full_bar[stage]);
+        }
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
       }
     }
@@ -88,8 +94,6 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
   const bool ok = prm.status == SEL_OK;
   const float r_f = prm.r_f;
   const int minexp = prm.minexp;
-  unsigned int *const hlane = hist + (lane % Cfg::COPIES) * kHStride;
-  unsigned int *const htrash = hist + Cfg::COPIES * kHStride;   // inactive lanes count here
   unsigned int ovf = 0;
   int stage = 0;
   uint32_t ph = 0;
@@ -101,16 +105,23 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
     const float *S = base + stage * Cfg::STAGE_FLOATS;
     uint64_t tbits = 0;
     double terr = 0.0;
-    tile_consume<D, DBG>(S, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hlane, htrash, tbl,
-                         &s_tbl_used, 1, ws.hist, ovf, dbg, tbits, terr);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[stage]);      // stage free for the producer
+    if constexpr (Cfg::DIRECT) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[stage]);    // descriptor read: slot free
+      tile_consume_direct<DBG>(x, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hist, ws.hist,
+                               ovf, dbg, tbits, terr);
+    } else {
+      tile_consume<D, DBG>(S, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hist, ws.hist, ovf,
+                           dbg, tbits, terr);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[stage]);    // stage free for the producer
+    }
     task_store(ws.task_part, t * CW + warp, tbits, terr);
     if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
   }
   ovf_flush(ovf, ws.hist);
   consumer_sync<CW * 32>();
-  tile_hist_flush<D>(hist, tbl, &s_tbl_used, 1, ws.hist, threadIdx.x, CW * 32);
+  tile_hist_flush<D>(hist, ws.hist, threadIdx.x, CW * 32);
 }
 
 // ============================================================ host side
@@ -195,7 +206,8 @@ int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Worksp
   if (dbg) d = *dbg;
   TileGeo tg = tl.tg;
   Workspace w = ws;
-  void *args[] = {(void *)&map, (void *)&tg, (void *)&w, (void *)&d};
+  const float *xp = x;
+  void *args[] = {(void *)&map, (void *)&xp, (void *)&tg, (void *)&w, (void *)&d};
   const void *fn = rank == 3 ? tile_fn<3>(dbg != nullptr) : tile_fn<2>(dbg != nullptr);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tl.ctas);

@@ -17,43 +17,56 @@ namespace sel {
 #ifndef SEL_STAGES2
 #define SEL_STAGES2 3
 #endif
-#ifndef SEL_TB2
-#define SEL_TB2 8192
+#ifndef SEL_W2
+#define SEL_W2 16384           // shared-memory histogram window (bins), 2D
+#endif
+#ifndef SEL_W3
+#define SEL_W3 12288           // 3D
+#endif
+#ifndef SEL_DIRECT3
+#define SEL_DIRECT3 0          // 1: 3D tiles read straight from L2 into registers (no smem stage)
 #endif
 #ifndef SEL_CW3
-#define SEL_CW3 8
+#define SEL_CW3 (SEL_DIRECT3 ? 14 : 8)
 #endif
 #ifndef SEL_STAGES3
-#define SEL_STAGES3 2
+#define SEL_STAGES3 (SEL_DIRECT3 ? 4 : 2)
 #endif
-#ifndef SEL_TB3
-#define SEL_TB3 8704
+#ifndef SEL_RSTAGE3
+#define SEL_RSTAGE3 8192       // direct 3D: floats per stage (range chunks only)
 #endif
 
 constexpr int kBoxK = 4 * 32 + 4;             // 132 floats: 4 halo columns (last one used) + 128
-constexpr int kHBins = 1024;                  // histogram window: codes [-512, 512)
-constexpr int kHStride = kHBins + 1;          // copy stride (words): copy c of a bin -> bank + c
-constexpr uint32_t kHOff = kSlotOff + (uint32_t)(kCenter - kHBins / 2);
+constexpr int kChunk = 1024;                  // window flush granule (bins)
 
 template <int D>
 struct TileCfg {
+  // DIRECT: a tile task carries no staged data; each lane loads its block (+ halo) from
+  // global memory (L2: the producer prefetches the tile box) into registers.  Without the
+  // 2 x 87 KB smem stages of the 3D box the CTA can run as many consumer warps as the
+  // register file allows (3D is latency-bound: throughput scales with warps).
+  static constexpr bool DIRECT = D == 3 && SEL_DIRECT3;
   static constexpr int CW = D == 3 ? SEL_CW3 : SEL_CW2;           // consumer warps
   static constexpr int THREADS = (CW + 1) * 32;
   static constexpr int BOXJ = 4 * CW + 1;                         // halo row + 4 per warp
   static constexpr int BOXI = D == 3 ? 5 : 1;                     // halo plane + 4 (3D)
   static constexpr int PLANE = kBoxK * BOXJ;                      // floats per smem plane
   static constexpr uint32_t STAGE_BYTES = PLANE * BOXI * 4;
-  static constexpr int STAGE_FLOATS = ((STAGE_BYTES + 127) & ~127) / 4;
+  // direct: the stages only carry range chunks (cp.async.bulk), tile tasks no data
+  static constexpr int STAGE_FLOATS = DIRECT ? SEL_RSTAGE3 : ((STAGE_BYTES + 127) & ~127) / 4;
   static constexpr int STAGES = D == 3 ? SEL_STAGES3 : SEL_STAGES2;
-  static constexpr int COPIES = D == 3 ? 4 : 8;                   // histogram lane copies
-  static constexpr int HIST_WORDS = (COPIES + 1) * kHStride;   // + trash copy
-  // second level: one table of TB 32-bit counters centred on code 0 for the codes
-  // outside the lane-copy window (wide distributions: noise, fronts, coarse data)
-  static constexpr int TB = D == 3 ? SEL_TB3 : SEL_TB2;
-  static constexpr int TBL_WORDS = TB;
-  static constexpr uint32_t kTOff = kSlotOff + (uint32_t)(kCenter - TB / 2);   // bits -> table slot
+  // One CTA-wide histogram window of W u32 bins in shared memory, codes [-W/2, W/2),
+  // one copy: smem atomic increments with unused results compile to ATOMS.POPC.INC,
+  // which merges the lanes of a warp that hit the same bin (measured: 1 copy is as fast
+  // as 2 or 8 lane-replicated copies on the smooth configs).  Word W is the pad bin that
+  // out-of-window codes (counted by the far path) and inactive lanes increment.
+  static constexpr int W = D == 3 ? SEL_W3 : SEL_W2;
+  static constexpr int HIST_WORDS = W + 4;
+  static constexpr uint32_t kWOff = kSlotOff + (uint32_t)(kCenter - W / 2);   // bits(q+M) -> bin
   static constexpr size_t SMEM = 128 + (size_t)STAGES * STAGE_FLOATS * 4 + HIST_WORDS * 4 +
-                                 TBL_WORDS * 4 + STAGES * 48 + 16;
+                                 STAGES * 48 + 16;
+  static_assert(W % kChunk == 0 && (kCenter - W / 2 + 1) % 4 == 0, "window alignment");
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 // ------------------------------------------------------------ mbarrier / TMA PTX
@@ -143,26 +156,49 @@ __device__ __forceinline__ void load_plane(const float *prow, int lane, float (&
 }
 
 // SZ code of one residual: b = bits(q + M) (reading R5, see sel_device.cuh), w = its
-// offset in the window; one unconditional increment of the lane's copy (no divergence):
-// out-of-window values land in the copy's pad word (index kHBins), ignored at the flush.
-__device__ __forceinline__ uint32_t sz_win(float d, float r_f, unsigned int *hcopy) {
+// bin in the window; one unconditional increment (no divergence): out-of-window values
+// (and every value of a lane whose r_f is NaN, i.e. an inactive lane) land in the pad bin
+// W, ignored at the flush.
+template <int D>
+__device__ __forceinline__ uint32_t sz_win(float d, float r_f, unsigned int *win) {
   const uint32_t b = __float_as_uint(__fadd_rn(__fmul_rn(d, r_f), kMagic));
-  const uint32_t w = b - kHOff;
-  atomicAdd(hcopy + min(w, (uint32_t)kHBins), 1u);
+  const uint32_t w = b - TileCfg<D>::kWOff;
+  atomicAdd(win + min(w, (uint32_t)TileCfg<D>::W), 1u);
   return w;
+}
+
+// Codes of one row of 4 that fell outside the window (wide distributions: noise, fronts):
+// one warp-uniform branch per row; each goes to the global histogram, or to the overflow
+// count (slot 65,535, R5).  act: the lane's values are real SZ points.
+template <int D, typename GH>
+__device__ __forceinline__ void sz_far(const uint32_t (&w)[4], uint32_t any, bool act, GH *ghist,
+                                       unsigned int &ovf) {
+  using Cfg = TileCfg<D>;
+  if (__any_sync(0xffffffffu, act && any >= (uint32_t)Cfg::W)) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (act && w[c] >= (uint32_t)Cfg::W) {
+        const uint32_t sl = w[c] + (Cfg::kWOff - kSlotOff);
+        if (sl > 65534u) ++ovf;
+        else atomicAdd(ghist + sl, (GH)1);
+      }
+  }
+}
+
+__device__ __forceinline__ float lane_rf(bool act, float r_f) {   // NaN: every code -> pad bin
+  return act ? r_f : __uint_as_float(0x7fc00000u);
 }
 
 
 // Consumer work of one tile task (block-layer bi, tile row btj, tile column btk; warp-level:
 // every consumer warp of the CTA calls it for the same tile).  S: the tile's smem stage.  Adds the SZ codes to the CTA's histogram
 // (lane copies / packed table / ghist / ovf) and returns the lane's block bits/error.
-template <int D, bool DBG>
+template <int D, bool DBG, typename GH = unsigned long long>
 __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, int bi,
                                              const TileGeo &tg, int warp,
                                              int lane, bool ok, float r_f, int minexp,
-                                             unsigned int *hlane, unsigned int *htrash,
-                                             unsigned int *tbl, int *tbl_used, int tbl_mark,
-                                             unsigned long long *ghist,
+                                             unsigned int *win,
+                                             GH *ghist,
                                              unsigned int &ovf, const DebugPtrs &dbg,
                                              uint64_t &tbits, double &terr) {
   using Cfg = TileCfg<D>;
@@ -180,7 +216,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
       const bool activeK = bk < tg.nb[2];
       const int I0 = 4 * bi, J0 = 4 * bj, K0 = 4 * bk;
       const float *wrow = S + (4 * warp) * kBoxK;   // smem row of j = J0 - 1 (plane 0)
-      unsigned int *const hcopy = activeK ? hlane : htrash;
+      const float rf = lane_rf(activeK, r_f);
       // ---------------- SZ: nested differences on the tile (R4), codes -> histogram (R5)
       float dprev[4][4];
 #pragma unroll
@@ -234,13 +270,13 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
             } else {
               d = d2;
             }
-            w[c] = sz_win(d, r_f, hcopy);
+            w[c] = sz_win<D>(d, rf, win);
             any |= w[c];
           }
           // the field origin is stored verbatim, not coded (R4): undo its count
           const bool orow = (i == 0) && (j == 0) && (btk == 0);
           if (orow && lane == 0) {
-            if (w[0] < (uint32_t)kHBins) atomicSub(hcopy + w[0], 1u);
+            if (w[0] < (uint32_t)Cfg::W) atomicSub(win + w[0], 1u);
             w[0] = 0u;
           }
           if constexpr (DBG) {
@@ -248,34 +284,12 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 if (orow && lane == 0 && c == 0) continue;
-                const uint32_t sl = w[c] + (kHOff - kSlotOff);
+                const uint32_t sl = w[c] + (Cfg::kWOff - kSlotOff);
                 dbg.codes[((int64_t)i * n1 + j) * n2 + K0 + c] = sl > 65534u ? kOvfSlot : (int32_t)sl;
               }
             }
           }
-          // out-of-window codes (wide distributions): one warp-uniform branch per row; the
-          // table takes them with one predicated atomic each, the rest (rare) go to the
-          // global histogram or the overflow count
-          if (__any_sync(0xffffffffu, activeK && any >= (uint32_t)kHBins)) {
-            uint32_t far = 0u;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const uint32_t tb = w[c] + (kHOff - Cfg::kTOff);
-              const bool out = activeK && w[c] >= (uint32_t)kHBins;
-              if (out && tb < (uint32_t)Cfg::TB) atomicAdd(tbl + tb, 1u);
-              far |= (out && tb >= (uint32_t)Cfg::TB) ? (1u << c) : 0u;
-            }
-            if (lane == 0) *tbl_used = tbl_mark;
-            if (__any_sync(0xffffffffu, far != 0u)) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (far & (1u << c)) {
-                  const uint32_t sl = w[c] + (kHOff - kSlotOff);
-                  if (sl > 65534u) ++ovf;
-                  else atomicAdd(ghist + sl, 1ull);
-                }
-            }
-          }
+          sz_far<D>(w, any, activeK, ghist, ovf);
         }
       }
       // ---------------- ZFP on the lane's block, edge-replicated at the far edges (R17)
@@ -317,22 +331,176 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
     }
 }
 
+// Direct 3D tile task (TileCfg<3>::DIRECT): same work and results as tile_consume, but
+// the lane's 4x4x4 block, the -1 halo plane / row of the warp's block row and the left
+// neighbour column come from global memory (L2) instead of a TMA-staged smem tile.  All
+// lanes of a warp share (I0, J0), so a row's left neighbour (k = K0 - 1) is the previous
+// lane's last column (SHFL); lane 0 loads it (zero at k = 0, R4).  Rows / planes past the
+// field's far edge are clamped (edge replication for ZFP, R17) and carry no SZ point.
+__device__ __forceinline__ float4 ldg4(const float *p) {
+  return __ldg(reinterpret_cast<const float4 *>(p));
+}
+
+template <bool DBG, typename GH>
+__device__ __forceinline__ void tile_consume_direct(const float *__restrict__ x, int btk, int btj,
+                                                    int bi, const TileGeo &tg, int warp, int lane,
+                                                    bool ok, float r_f, int minexp,
+                                                    unsigned int *win,
+                                                    GH *ghist, unsigned int &ovf,
+                                                    const DebugPtrs &dbg, uint64_t &tbits,
+                                                    double &terr) {
+  using Cfg = TileCfg<3>;
+  constexpr int CW = Cfg::CW;
+  const int n0 = (int)tg.n[0], n1 = (int)tg.n[1], n2 = (int)tg.n[2];
+  const int bj = btj * CW + warp;
+  const int bk0 = btk * 32 + lane;
+  tbits = 0;
+  terr = 0.0;
+  if (!ok || bj >= tg.nb[1]) return;                    // warp-uniform
+  const bool activeK = bk0 < tg.nb[2];
+  const int bk = activeK ? bk0 : tg.nb[2] - 1;          // inactive lanes: a valid block
+  const int I0 = 4 * bi, J0 = 4 * bj, K0 = 4 * bk;
+  const float rf = lane_rf(activeK, r_f);
+  auto row = [&](int i, int j) -> const float * { return x + ((int64_t)i * n1 + j) * n2; };
+  // previous lane's last column = this lane's k = K0 - 1 (lane 0: load, 0 at k = 0)
+  auto left = [&](float v3, const float *r) -> float {
+    const float s = __shfl_up_sync(0xffffffffu, v3, 1);
+    return lane == 0 ? (K0 > 0 ? __ldg(r + K0 - 1) : 0.0f) : s;
+  };
+  // the block, edge-replicated (R17)
+  float blk[64];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int ic = min(I0 + p, n0 - 1);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 q = ldg4(row(ic, min(J0 + r, n1 - 1)) + K0);
+      const int o = (p * 4 + r) * 4;
+      blk[o] = q.x; blk[o + 1] = q.y; blk[o + 2] = q.z; blk[o + 3] = q.w;
+    }
+  }
+  // ---------------- SZ: nested differences (R4), codes -> histogram (R5)
+  float dprev[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dprev[r][c] = 0.0f;
+  if (I0 > 0) {                  // plane i = I0 - 1: its D2 differences (zeros at i < 0)
+    const int i = I0 - 1;
+    float d1up[4];
+    {
+      float u[4] = {0.f, 0.f, 0.f, 0.f};
+      float hl = 0.0f;
+      if (J0 > 0) {
+        const float *rp = row(i, J0 - 1);
+        const float4 q = ldg4(rp + K0);
+        u[0] = q.x; u[1] = q.y; u[2] = q.z; u[3] = q.w;
+        hl = left(u[3], rp);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) d1up[c] = u[c] - (c ? u[c - 1] : hl);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float *rp = row(i, min(J0 + r, n1 - 1));
+      const float4 q = ldg4(rp + K0);
+      const float v[4] = {q.x, q.y, q.z, q.w};
+      const float hl = left(v[3], rp);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float d1 = v[c] - (c ? v[c - 1] : hl);
+        dprev[r][c] = d1 - d1up[c];
+        d1up[c] = d1;
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int i = I0 + p;
+    if (i >= n0) break;                                  // padded planes: no SZ point
+    float d1up[4];
+    {
+      float u[4] = {0.f, 0.f, 0.f, 0.f};
+      float hl = 0.0f;
+      if (J0 > 0) {
+        const float *rp = row(i, J0 - 1);
+        const float4 q = ldg4(rp + K0);
+        u[0] = q.x; u[1] = q.y; u[2] = q.z; u[3] = q.w;
+        hl = left(u[3], rp);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) d1up[c] = u[c] - (c ? u[c - 1] : hl);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int j = J0 + r;
+      if (j >= n1) break;                                // padded rows: no SZ point
+      const float *v = blk + (p * 4 + r) * 4;
+      const float hl = left(v[3], row(i, j));
+      uint32_t w[4];
+      uint32_t any = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float d1 = v[c] - (c ? v[c - 1] : hl);
+        const float d2 = d1 - d1up[c];
+        d1up[c] = d1;
+        const float d = d2 - dprev[r][c];
+        dprev[r][c] = d2;
+        w[c] = sz_win<3>(d, rf, win);
+        any |= w[c];
+      }
+      // the field origin is stored verbatim, not coded (R4): undo its count
+      const bool orow = (i == 0) && (j == 0) && (btk == 0);
+      if (orow && lane == 0) {
+        if (w[0] < (uint32_t)Cfg::W) atomicSub(win + w[0], 1u);
+        w[0] = 0u;
+      }
+      if constexpr (DBG) {
+        if (activeK) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (orow && lane == 0 && c == 0) continue;
+            const uint32_t sl = w[c] + (Cfg::kWOff - kSlotOff);
+            dbg.codes[((int64_t)i * n1 + j) * n2 + K0 + c] = sl > 65534u ? kOvfSlot : (int32_t)sl;
+          }
+        }
+      }
+      sz_far<3>(w, any, activeK, ghist, ovf);
+    }
+  }
+  // ---------------- ZFP on the lane's block (already edge-replicated)
+  if (activeK) {
+    uint32_t bits;
+    double E;
+    int emax;
+    int cf[64];
+    uint32_t u[64];
+    zfp_block<3, DBG>(blk, minexp, bits, E, emax, cf, u);
+    tbits = bits;
+    terr = E;
+    if constexpr (DBG) {
+      const int64_t tb = ((int64_t)bi * tg.nb[1] + bj) * tg.nb[2] + bk;
+      dbg.emax[tb] = emax; dbg.bits[tb] = bits; dbg.err[tb] = E;
+#pragma unroll
+      for (int n = 0; n < 64; ++n) { dbg.coef[tb * 64 + n] = cf[n]; dbg.uword[tb * 64 + n] = u[n]; }
+    }
+  }
+}
+
 // Sampled-block task (strides > 1; k_batch): lane = processed block t (act: t < n_pb),
 // read with its halo from global memory (L2: the range pass just streamed the field),
 // codes into the same smem histogram as a tile task, ZFP block in registers.  Every lane
 // of the warp runs (inactive lanes on a clamped block, contributing nothing) so the
 // warp-uniform out-of-window branch stays uniform.
-template <int D>
+template <int D, typename GH>
 __device__ __forceinline__ void sampled_consume(const float *__restrict__ x, const Geo &g,
                                                 int64_t t, bool act, float r_f, int minexp,
-                                                unsigned int *hlane, unsigned int *htrash,
-                                                unsigned int *tbl, int *tbl_used, int tbl_mark,
-                                                unsigned long long *ghist, unsigned int &ovf,
+                                                unsigned int *win,
+                                                GH *ghist, unsigned int &ovf,
                                                 uint64_t &tbits, double &terr) {
   using Cfg = TileCfg<D>;
   constexpr int SZ = Tab<D>::SIZE;
   constexpr int PL = D == 3 ? 4 : 1;
-  const int lane = threadIdx.x & 31;
   if (!act) t = 0;
   const int64_t p2 = t % g.npb[2];
   const int64_t qq = t / g.npb[2];
@@ -395,30 +563,11 @@ __device__ __forceinline__ void sampled_consume(const float *__restrict__ x, con
           d = d2;
         }
         const bool valid = rowok && !(i == 0 && j == 0 && K0 + c == 0);   // origin (R4)
-        w[c] = sz_win(d, r_f, valid ? hlane : htrash);
+        w[c] = sz_win<D>(d, valid ? r_f : __uint_as_float(0x7fc00000u), win);
         w[c] = valid ? w[c] : 0u;
         any |= w[c];
       }
-      if (__any_sync(0xffffffffu, any >= (uint32_t)kHBins)) {
-        uint32_t far = 0u;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint32_t tb = w[c] + (kHOff - Cfg::kTOff);
-          const bool out = w[c] >= (uint32_t)kHBins;
-          if (out && tb < (uint32_t)Cfg::TB) atomicAdd(tbl + tb, 1u);
-          far |= (out && tb >= (uint32_t)Cfg::TB) ? (1u << c) : 0u;
-        }
-        if (lane == 0) *tbl_used = tbl_mark;
-        if (__any_sync(0xffffffffu, far != 0u)) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (far & (1u << c)) {
-              const uint32_t sl = w[c] + (kHOff - kSlotOff);
-              if (sl > 65534u) ++ovf;
-              else atomicAdd(ghist + sl, 1ull);
-            }
-        }
-      }
+      sz_far<D>(w, any, true, ghist, ovf);
     }
   }
   uint32_t bits;
@@ -431,31 +580,17 @@ __device__ __forceinline__ void sampled_consume(const float *__restrict__ x, con
   terr = act ? E : 0.0;
 }
 
-// Move the CTA's smem histogram (lane copies + packed table) into the global histogram
-// and clear it.  Called by the consumer threads (tid < nthr) after a consumer barrier.
+// Move the CTA's smem window into the global (u64) histogram and clear it (k_tile, at
+// the end of its field).  Called by the consumer threads (tid < nthr) after a barrier.
 template <int D>
-__device__ __forceinline__ void tile_hist_flush(unsigned int *hist, unsigned int *tbl,
-                                                const int *tbl_used, int tbl_mark,
-                                                unsigned long long *ghist,
-                                                int tid, int nthr) {
+__device__ __forceinline__ void tile_hist_flush(unsigned int *win, unsigned long long *ghist, int tid,
+                                                int nthr) {
   using Cfg = TileCfg<D>;
-  for (int i = tid; i < kHBins; i += nthr) {
-    unsigned long long c = 0;
-#pragma unroll
-    for (int k = 0; k < Cfg::COPIES; ++k) {
-      c += hist[k * kHStride + i];
-      hist[k * kHStride + i] = 0u;
-    }
-    if (c) atomicAdd(ghist + (kCenter - kHBins / 2) + i, c);
-  }
-  // the flag holds the mark of the last flush interval that used the table (a mark per
-  // interval, so nobody has to reset it between a flush and the next codes)
-  if (*tbl_used != tbl_mark) return;    // no code outside the lane-copy window: table is zero
-  for (int i = tid; i < Cfg::TB; i += nthr) {
-    const uint32_t v = tbl[i];
-    if (v) {
-      tbl[i] = 0u;
-      atomicAdd(ghist + (kCenter - Cfg::TB / 2) + i, (unsigned long long)v);
+  for (int i = tid; i < Cfg::W; i += nthr) {
+    const unsigned int c = win[i];
+    if (c) {
+      win[i] = 0u;
+      atomicAdd(ghist + (kCenter - Cfg::W / 2) + i, (unsigned long long)c);
     }
   }
 }

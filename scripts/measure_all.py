@@ -1,6 +1,6 @@
 """Throughput of k_batch on every BASELINE config (developer tool; writes a markdown table).
 
-    python scripts/measure_all.py > gpurun_out/throughput.md
+    python scripts/measure_all.py [c1,c2,c3,c4,c5] > gpurun_out/throughput.md
 Fields already in HBM, steps = one sel_estimate_batch_async of the whole stack + D2H of
 the results, CUDA events, 2 warm-up + 5 timed steps; GB/s = float32 input bytes / time.
 """
@@ -33,25 +33,30 @@ def run(fields, eb, stride, label):
     p.close()
 
 
+SEL = set((sys.argv[1] if len(sys.argv) > 1 else "c1,c2,c3,c4,c5").split(","))
 print(f"| workload | fields | eb_rel | stride | us / field | GB/s | % of HBM ({PEAK:g} GB/s) | SZ / ZFP chosen |")
 print("|---|---:|---:|---|---:|---:|---:|---|")
-f1 = [torch.from_numpy(synth.c1_field(seed=i)).cuda() for i in range(256)]
-run(f1, 1e-4, None, "C1 256x256 (x256 seeds)")
-del f1
-f2 = [torch.from_numpy(synth.make_field(2, i)).cuda() for i in range(100)]
-run(f2, 1e-4, None, "C2 1800x3600")
-run(f2, 1e-4, (1, 10), "C2 1800x3600")
-del f2
-f3 = [torch.from_numpy(synth.make_field(3, i)).cuda() for i in range(13)]
-for eb in (1e-3, 1e-4, 1e-5):
+if "c1" in SEL:
+  f1 = [torch.from_numpy(synth.c1_field(seed=i)).cuda() for i in range(256)]
+  run(f1, 1e-4, None, "C1 256x256 (x256 seeds)")
+  del f1
+if "c2" in SEL:
+  f2 = [torch.from_numpy(synth.make_field(2, i)).cuda() for i in range(100)]
+  run(f2, 1e-4, None, "C2 1800x3600")
+  run(f2, 1e-4, (1, 10), "C2 1800x3600")
+  del f2
+if "c3" in SEL:
+  f3 = [torch.from_numpy(synth.make_field(3, i)).cuda() for i in range(13)]
+  for eb in (1e-3, 1e-4, 1e-5):
     run(f3, eb, None, "C3 100x500x500")
-del f3
-f4 = [torch.from_numpy(synth.make_field(4, i)).cuda() for i in range(6)]
-run(f4, 1e-4, None, "C4 512^3")
-run(f4, 1e-4, (4, 4, 4), "C4 512^3")
-del f4
-torch.cuda.empty_cache()
-for mix in (0, 1, 2):
+  del f3
+if "c4" in SEL:
+  f4 = [torch.from_numpy(synth.make_field(4, i)).cuda() for i in range(6)]
+  run(f4, 1e-4, None, "C4 512^3")
+  run(f4, 1e-4, (4, 4, 4), "C4 512^3")
+  del f4
+  torch.cuda.empty_cache()
+for mix in ((0, 1, 2) if "c5" in SEL else ()):
     t0 = time.time()
     x = torch.from_numpy(synth.make_field(5, mix)).cuda()
     for eb in (1e-2, 1e-4, 1e-6):
