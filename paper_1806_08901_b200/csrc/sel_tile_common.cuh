@@ -18,7 +18,7 @@ namespace sel {
 #define SEL_STAGES2 3
 #endif
 #ifndef SEL_W2
-#define SEL_W2 16384           // shared-memory histogram window (bins), 2D
+#define SEL_W2 8192            // shared-memory histogram window (bins), 2D
 #endif
 #ifndef SEL_W3
 #define SEL_W3 12288           // 3D
@@ -237,25 +237,16 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
             d1up[c] = d1;
           }
       }
+      // Blocks away from the far edges and the field origin (warp-uniform) skip the per-row
+      // bound / origin checks and the edge replication.
+      const bool edge = J0 + 4 > n1 || (D == 3 && I0 + 4 > n0) || (btk == 0 && J0 == 0 && I0 == 0);
       float blk2[D == 2 ? 16 : 1];   // 2D: the ZFP block is rows 1..4 of the SZ plane
-#pragma unroll 1
-      for (int p = 0; p < NPL; ++p) {
-        const int i = I0 + p;
-        float v[5][4], h[5], d1up[4];
-        load_plane(wrow + (D == 3 ? (p + 1) * Cfg::PLANE : 0), lane, v, h);
-        if constexpr (D == 2) {       // rows past the field's edge replicate the last (R17)
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              blk2[4 * r + c] = (r == 0 || J0 + r < n1) ? v[r + 1][c] : blk2[4 * (r - 1) + c];
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) d1up[c] = v[0][c] - (c ? v[0][c - 1] : h[0]);
+      auto rows = [&](auto EDGE, int i, const float (&v)[5][4], const float (&h)[5], float (&d1up)[4]) {
+        constexpr bool E = decltype(EDGE)::value;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int j = J0 + r;
-          if (i >= n0 || j >= n1) break;              // padded rows/planes: no SZ point
+          if (E && (i >= n0 || j >= n1)) break;       // padded rows/planes: no SZ point
           uint32_t w[4];
           uint32_t any = 0;
 #pragma unroll
@@ -274,7 +265,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
             any |= w[c];
           }
           // the field origin is stored verbatim, not coded (R4): undo its count
-          const bool orow = (i == 0) && (j == 0) && (btk == 0);
+          const bool orow = E && (i == 0) && (j == 0) && (btk == 0);
           if (orow && lane == 0) {
             if (w[0] < (uint32_t)Cfg::W) atomicSub(win + w[0], 1u);
             w[0] = 0u;
@@ -291,6 +282,23 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
           }
           sz_far<D>(w, any, activeK, ghist, ovf);
         }
+      };
+#pragma unroll 1
+      for (int p = 0; p < NPL; ++p) {
+        const int i = I0 + p;
+        float v[5][4], h[5], d1up[4];
+        load_plane(wrow + (D == 3 ? (p + 1) * Cfg::PLANE : 0), lane, v, h);
+        if constexpr (D == 2) {       // rows past the field's edge replicate the last (R17)
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              blk2[4 * r + c] = (r == 0 || !edge || J0 + r < n1) ? v[r + 1][c] : blk2[4 * (r - 1) + c];
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) d1up[c] = v[0][c] - (c ? v[0][c - 1] : h[0]);
+        if (edge) rows(std::true_type{}, i, v, h, d1up);
+        else rows(std::false_type{}, i, v, h, d1up);
       }
       // ---------------- ZFP on the lane's block, edge-replicated at the far edges (R17)
       if (activeK) {
