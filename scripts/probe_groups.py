@@ -12,10 +12,13 @@ for cfg, nf in (((2, 100), (3, 10), (1, 256)) if len(sys.argv) < 2 else [tuple(m
     p = sel.Plan(shape, eb, "rel")
     buf = p.results_buffer(nf)
     ref = None
-    for G in (((0, 1, 2, 3, 4) if cfg != 1 else (0, 4, 8, 12, 16, 24)) if os.environ.get("SWEEP_G") else (0,)):
+    lags = [int(v) for v in os.environ.get("SWEEP_LAG", "1").split(",")]
+    Gs = ((0, 1, 2, 3, 4) if cfg != 1 else (0, 4, 8, 12, 16, 24)) if os.environ.get("SWEEP_G") else (0,)
+    for lag, G in [(l, g) for l in lags for g in Gs]:
         if G > nf:
             continue
         p.set_option("groups", G)
+        p.set_option("lag", lag)
         for _ in range(2):
             p.estimate_batch_async(fields, buf)
         torch.cuda.synchronize()
@@ -30,6 +33,6 @@ for cfg, nf in (((2, 100), (3, 10), (1, 256)) if len(sys.argv) < 2 else [tuple(m
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 5
         gbs = nf * fields[0].numel() * 4 / ms / 1e6
-        print(f"C{cfg} nf={nf} G={G}: {ms/nf*1000:.1f} us/field {gbs:.0f} GB/s identical={same}", flush=True)
+        print(f"C{cfg} nf={nf} lag={lag} G={G}: {ms/nf*1000:.1f} us/field {gbs:.0f} GB/s identical={same}", flush=True)
     p.close()
     del fields
