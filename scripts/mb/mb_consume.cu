@@ -10,7 +10,7 @@ using namespace sel;
 
 template <int D>
 __global__ void __launch_bounds__(TileCfg<D>::CW * 32, 1)
-    k_mb(int iters, float r_f, int minexp, float amp, unsigned int *gh, unsigned long long *sink) {
+    k_mb(int iters, float r_f, int minexp, float amp, float noise, unsigned int *gh, unsigned long long *sink) {
   using Cfg = TileCfg<D>;
   extern __shared__ float sm[];
   float *S = sm;
@@ -18,7 +18,10 @@ __global__ void __launch_bounds__(TileCfg<D>::CW * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < Cfg::STAGE_FLOATS; i += blockDim.x) {
     const float t = (float)i;
-    S[i] = amp * (sinf(t * 0.013f) + 0.5f * cosf(t * 0.0071f + (float)blockIdx.x)) + 1e-3f * sinf(t * 1.7f);
+    unsigned h = (unsigned)i * 2654435761u + blockIdx.x * 40503u;
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    const float u = (float)(h & 0xffffff) / 16777216.0f - 0.5f;
+    S[i] = amp * (sinf(t * 0.013f) + 0.5f * cosf(t * 0.0071f + (float)blockIdx.x)) + noise * u;
   }
   for (int i = threadIdx.x; i < Cfg::HIST_WORDS; i += blockDim.x) win[i] = 0u;
   __syncthreads();
@@ -42,7 +45,7 @@ __global__ void __launch_bounds__(TileCfg<D>::CW * 32, 1)
 }
 
 template <int D>
-void run(float r_f, int minexp, float amp, const char *label) {
+void run(float r_f, int minexp, float amp, float noise, const char *label) {
   using Cfg = TileCfg<D>;
   const size_t smem = (size_t)Cfg::STAGE_FLOATS * 4 + Cfg::HIST_WORDS * 4;
   cudaFuncSetAttribute(k_mb<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -52,11 +55,11 @@ void run(float r_f, int minexp, float amp, const char *label) {
   cudaMalloc(&gh, 70000 * 4);
   cudaMalloc(&sink, (1 + sms * Cfg::CW * 32) * 8);
   const int iters = D == 3 ? 200 : 2000;
-  k_mb<D><<<sms, Cfg::CW * 32, smem>>>(10, r_f, minexp, amp, gh, sink);
+  k_mb<D><<<sms, Cfg::CW * 32, smem>>>(10, r_f, minexp, amp, noise, gh, sink);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k_mb<D><<<sms, Cfg::CW * 32, smem>>>(iters, r_f, minexp, amp, gh, sink);
+  k_mb<D><<<sms, Cfg::CW * 32, smem>>>(iters, r_f, minexp, amp, noise, gh, sink);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -68,9 +71,13 @@ void run(float r_f, int minexp, float amp, const char *label) {
 
 int main() {
   // r_f: codes of a smooth field (spread ~ +-100) and of a rough one (~ +-3000)
-  run<2>(2000.f, -12, 1.0f, "smooth");
-  run<2>(2000.f, -12, 30.0f, "wide codes");
-  run<3>(2000.f, -12, 1.0f, "smooth");
-  run<3>(2000.f, -12, 30.0f, "wide codes");
+  // codes of noise of amplitude a: |code| ~ a * r_f (spread over +- a r_f bins)
+  run<2>(2000.f, -12, 1.0f, 1e-3f, "smooth");
+  run<2>(2000.f, -12, 1.0f, 0.05f, "noise +-100 codes");
+  run<2>(2000.f, -12, 1.0f, 0.5f, "noise +-1000 codes");
+  run<2>(2000.f, -12, 1.0f, 2.0f, "noise +-4000 codes");
+  run<3>(2000.f, -12, 1.0f, 1e-3f, "smooth");
+  run<3>(2000.f, -12, 1.0f, 0.05f, "noise +-100 codes");
+  run<3>(2000.f, -12, 1.0f, 0.5f, "noise +-1000 codes");
   return 0;
 }
