@@ -82,7 +82,8 @@ typedef struct {
   int32_t minexp;            /* floor(log2 eb_abs)                                            */
   float r_f;                 /* float(1/(2 eb_abs)), the quantiser scale                      */
   int32_t status;            /* sel_status of this field (batch calls)                        */
-  int32_t reserved;
+  int32_t choice_eb;         /* selection based on the error bound (Lu et al.): the  */
+                             /* lower bit-rate at the user's eb, 0 = SZ iff BR_sz < BR_zfp    */
 } sel_result;
 
 /* Create a plan for fields of shape dims[0..ndims-1].
@@ -145,6 +146,12 @@ int sel_estimate_batch_host(sel_plan_t plan, const float *const *h_fields, int n
  * (sz_bits_per_value, zfp_bits_per_value, zfp_psnr, zfp_mse, value_range, eb_abs).
  * Ties go to ZFP.  Errors: SEL_EINVAL (NULL). */
 int sel_choose(const sel_result *r, int32_t *choice);
+
+/* Pure host: the fixed-maximum-error selector the paper compares against (Lu et al.,
+ * P:639-642, "selects the compressor with the highest compression ratio based on a fixed
+ * error bound"): 0 (SZ) iff r->sz_bits_per_value < r->zfp_bits_per_value, both at the
+ * user's eb; ties go to ZFP as in Alg.1.  Equals r->choice_eb.  Errors: SEL_EINVAL (NULL). */
+int sel_choose_eb(const sel_result *r, int32_t *choice);
 
 /* Test-only: copy a debug dump of the LAST sel_estimate (requires option debug=1):
  *   "codes"  int32[N]           slot per point, -1 where no code was formed

@@ -65,7 +65,7 @@ class Result(C.Structure):
         ("sz_eb_matched", C.c_double), ("zfp_mse", C.c_double),
         ("n_sz_points", C.c_uint64), ("n_values", C.c_uint64), ("n_blocks", C.c_uint64),
         ("zfp_total_bits", C.c_uint64), ("zfp_err_sum", C.c_double),
-        ("minexp", C.c_int32), ("r_f", C.c_float),
+        ("minexp", C.c_int32), ("r_f", C.c_float), ("choice_eb", C.c_int32),
     ]
 
     def to_dict(self) -> dict:
@@ -125,6 +125,8 @@ def lib():
             L.orc_gain.restype = C.c_double
             L.orc_select.argtypes = [C.c_double] * 7 + [P, P, P]
             L.orc_select.restype = C.c_int
+            L.orc_select_eb.argtypes = [C.c_double, C.c_double]
+            L.orc_select_eb.restype = C.c_int
             _lib = L
     return _lib
 
@@ -275,3 +277,8 @@ def select(br_sz, psnr_sz, br_zfp, psnr_zfp, vr, eb_abs, zfp_mse):
     ch = lib().orc_select(br_sz, psnr_sz, br_zfp, psnr_zfp, vr, eb_abs, zfp_mse,
                           C.byref(bm), C.byref(ebm), C.byref(m))
     return int(ch), bm.value, ebm.value, int(m.value)
+
+
+def select_eb(br_sz, br_zfp):
+    """Selection based on the error bound (Lu et al.)."""
+    return int(lib().orc_select_eb(br_sz, br_zfp))

@@ -323,6 +323,18 @@ double orc_block_err(const int32_t *coef_nat, const uint32_t *u_seq, const int32
 }
 
 /* ------------------------------------------------------------------ */
+/* The comparison selector of P:639-642 (Lu et al., "selection based on  */
+/* error bound"): "simply selects the compressor with the highest        */
+/* compression ratio based on a fixed error bound" -- the lower bit-rate */
+/* at the user's eb (ratio = 32 / bit-rate for float32); ties -> ZFP as  */
+/* in Alg. 1's ELSE (reading; the paper does not discuss ties).          */
+/* ------------------------------------------------------------------ */
+int orc_select_eb(double br_sz, double br_zfp) {
+  double ratio_sz = 32.0 / br_sz, ratio_zfp = 32.0 / br_zfp;
+  return (ratio_sz > ratio_zfp) ? 0 : 1;
+}
+
+/* ------------------------------------------------------------------ */
 /* A16 selection, Alg. 1 lines 7-10, ties -> ZFP            */
 /* ------------------------------------------------------------------ */
 int orc_select(double br_sz, double psnr_sz, double br_zfp, double psnr_zfp,
@@ -502,6 +514,7 @@ int orc_estimate(const float *x, int nd, const int64_t *dims, int eb_mode, doubl
   out->r_f = r_f;
   out->choice = orc_select(br_sz, psnr_sz, br_zfp, psnr_zfp, VR, eb_abs, mse,
                            &out->sz_bits_matched, &out->sz_eb_matched, &out->matched);
+  out->choice_eb = orc_select_eb(br_sz, br_zfp);
   if (dbg && dbg->hist) memcpy(dbg->hist, hist, sizeof(uint64_t) * ORC_NSLOTS);
   free(hist);
   return ORC_OK;

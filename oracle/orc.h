@@ -36,6 +36,7 @@ typedef struct {
   double zfp_err_sum;   /* sum_b E_b (value units squared) */
   int32_t minexp;
   float r_f;
+  int32_t choice_eb;    /* selection based on the error bound (Lu et al.) */
 } orc_result;
 
 /* Optional per-element dumps (any pointer may be NULL).
@@ -82,6 +83,8 @@ uint64_t orc_gt_decode(const uint8_t *buf, uint64_t nbits, int n, int kmin, uint
 double orc_block_err(const int32_t *coef_nat, const uint32_t *u_seq, const int32_t *perm,
                      int ndims, int kmin, int32_t emax);
 double orc_gain(int ndims, int nat_index);
+/* selection based on the error bound: 0 = SZ iff its ratio is higher */
+int orc_select_eb(double br_sz, double br_zfp);
 int orc_select(double br_sz, double psnr_sz, double br_zfp, double psnr_zfp,
                double vr, double eb_abs, double zfp_mse, double *br_sz_matched,
                double *eb_sz_matched, int32_t *matched);

@@ -24,7 +24,7 @@ EB_ABS, EB_REL = 0, 1
 
 # every entry point declared in include/sel.h
 EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_batch",
-           "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_debug_copy", "sel_kernel_times",
+           "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_choose_eb", "sel_debug_copy", "sel_kernel_times",
            "sel_processed_blocks", "sel_processed_values", "sel_workspace_bytes",
            "sel_launch_count", "sel_plan_destroy", "sel_strerror")
 
@@ -47,11 +47,11 @@ class Result(C.Structure):
         ("n_sz_points", C.c_uint64), ("n_values", C.c_uint64), ("n_blocks", C.c_uint64),
         ("zfp_total_bits", C.c_uint64), ("zfp_err_sum", C.c_double),
         ("minexp", C.c_int32), ("r_f", C.c_float), ("status", C.c_int32),
-        ("reserved", C.c_int32),
+        ("choice_eb", C.c_int32),
     ]
 
     def to_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 _lib = None
@@ -80,6 +80,8 @@ def lib():
         L.sel_estimate_batch_host.restype = C.c_int
         L.sel_choose.argtypes = [C.POINTER(Result), C.POINTER(C.c_int32)]
         L.sel_choose.restype = C.c_int
+        L.sel_choose_eb.argtypes = [C.POINTER(Result), C.POINTER(C.c_int32)]
+        L.sel_choose_eb.restype = C.c_int
         L.sel_debug_copy.argtypes = [P, C.c_char_p, P, C.c_uint64]
         L.sel_debug_copy.restype = C.c_int
         L.sel_kernel_times.argtypes = [P, P, P, C.c_int]
@@ -272,4 +274,16 @@ def choose(result: dict) -> int:
             setattr(r, k, result[k])
     c = C.c_int32()
     _check(lib().sel_choose(C.byref(r), C.byref(c)))
+    return int(c.value)
+
+
+def choose_eb(result: dict) -> int:
+    """Host-side fixed-error-bound selector (Lu et al.): the compressor
+    with the lower bit-rate at the user's eb, ties to ZFP."""
+    r = Result()
+    for k, _ in Result._fields_:
+        if k in result:
+            setattr(r, k, result[k])
+    c = C.c_int32()
+    _check(lib().sel_choose_eb(C.byref(r), C.byref(c)))
     return int(c.value)

@@ -646,6 +646,12 @@ int sel_choose(const sel_result *r, int32_t *choice) {
   return SEL_OK;
 }
 
+int sel_choose_eb(const sel_result *r, int32_t *choice) {
+  if (!r || !choice) return SEL_EINVAL;
+  *choice = r->sz_bits_per_value < r->zfp_bits_per_value ? 0 : 1;   // P:639-642, ties -> ZFP
+  return SEL_OK;
+}
+
 int sel_debug_copy(sel_plan_t p, const char *what, void *dst, uint64_t bytes) {
   if (!p || !what || !dst || !p->dbg_mem) return SEL_EINVAL;
   const uint64_t N = (uint64_t)p->geo.N, B = (uint64_t)p->geo.n_pb, S = (uint64_t)p->size;

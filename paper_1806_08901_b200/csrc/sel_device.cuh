@@ -336,6 +336,8 @@ __device__ __forceinline__ sel_result assemble_result(const Params &prm, double 
   r.zfp_bits_per_value = (double)tb / (double)fa.n_values;
   r.zfp_mse = mse;
   r.zfp_psnr = mse > 0.0 ? 20.0 * lg_vr - 10.0 * lg_mse : __longlong_as_double(0x7ff0000000000000LL);
+  // selection based on the error bound (Lu et al.): lower bit-rate at eb
+  r.choice_eb = r.sz_bits_per_value < r.zfp_bits_per_value ? 0 : 1;
   if (!(r.zfp_mse > 0.0) || !(vr > 0.0) || !isfinite(r.zfp_psnr)) {
     r.matched = 0;
     r.sz_bits_matched = r.sz_bits_per_value;

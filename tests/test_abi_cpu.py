@@ -80,6 +80,17 @@ def test_choose_matches_oracle_selection(sel, orc):
         assert sel.choose(r) == ch
 
 
+def test_choose_eb_matches_oracle_selection(sel, orc):
+    """sel_choose_eb (host, the fixed-error-bound selector of P:639-642) agrees with the
+    oracle's, including ties (-> ZFP)."""
+    rng = np.random.default_rng(1)
+    for _ in range(2000):
+        br_sz = float(rng.uniform(0.5, 20))
+        br_zfp = br_sz if rng.random() < 0.1 else float(rng.uniform(0.1, 25))
+        r = dict(sz_bits_per_value=br_sz, zfp_bits_per_value=br_zfp)
+        assert sel.choose_eb(r) == orc.select_eb(br_sz, br_zfp)
+
+
 def test_product_path_has_no_oracle_dependency():
     """The product package never imports or links the oracle."""
     pkg = os.path.join(ROOT, "paper_1806_08901_b200")

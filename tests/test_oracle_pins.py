@@ -511,6 +511,32 @@ def test_selection_ties_and_unmatched(orc):
     assert m == 0 and ch == 1
 
 
+def test_fixed_error_bound_selector_differs_from_rate_distortion(orc):
+    """the selector of Lu et al. takes the higher compression ratio at the
+    user's eb; "ZFP may have a higher PSNR than does SZ, even if its compression ratio is
+    lower", which is where the rate-distortion selection (Alg. 1) disagrees with it."""
+    psnr_sz = 20 * math.log10(1.0 / 1e-4) + 10 * math.log10(3.0)
+    # ZFP 12.04 dB better than SZ at eb: SZ needs 2 more bits/value to match
+    ch, bm, _, m = orc.select(3.0, psnr_sz, 3.5, psnr_sz + 20 * math.log10(4.0), 1.0, 1e-4, 1e-9)
+    assert m == 1 and bm == pytest.approx(5.0, rel=1e-12) and ch == 1          # Alg. 1: ZFP
+    assert orc.select_eb(3.0, 3.5) == 0                                        # Lu et al.: SZ
+    assert orc.select_eb(3.5, 3.5) == 1                                        # tie -> ZFP
+    assert orc.select_eb(4.0, 3.5) == 1
+
+
+def test_fixed_error_bound_selector_on_fields(orc):
+    """choice_eb is the lower bit-rate at eb; where matching is impossible (MSE = 0) the
+    Alg. 1 fallback compares at eb too, so both selectors agree there."""
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((37, 45)).astype(np.float32)
+    r = orc.estimate(x, 1e-3)
+    assert r["choice_eb"] == (0 if r["sz_bits_per_value"] < r["zfp_bits_per_value"] else 1)
+    xi = rng.integers(-3, 4, (20, 24)).astype(np.float32)        # exact in fp32, MSE = 0 at kmin = 0
+    r = orc.estimate(xi, 2.0 ** -20, mode="abs")
+    assert r["matched"] == 0 and r["zfp_mse"] == 0.0
+    assert r["choice"] == r["choice_eb"]
+
+
 # ------------------------------------------------------ sampling (A3)
 def test_processed_block_counts(orc):
     assert orc.processed_blocks((1800, 3600), (1, 10)) == 40500

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 REL = 1e-6
-EXACT_KEYS = ("n_sz_points", "n_values", "n_blocks", "zfp_total_bits", "minexp", "r_f",
+EXACT_KEYS = ("n_sz_points", "n_values", "n_blocks", "zfp_total_bits", "minexp", "r_f", "choice_eb",
               "choice", "matched", "value_range", "eb_abs")
 CLOSE_KEYS = ("sz_entropy", "sz_bits_per_value", "sz_psnr", "zfp_bits_per_value", "zfp_psnr",
               "zfp_mse", "zfp_err_sum", "sz_bits_matched", "sz_eb_matched", "sz_overflow_frac")
