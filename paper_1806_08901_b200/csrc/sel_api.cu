@@ -58,6 +58,7 @@ struct sel_plan_st {
   int groups = 0;                 // k_batch CTA groups (0: auto, batch_groups)
   int lag_t = 2;                  // k_batch phases from a field's range pass to its tiles
   void *bstate = nullptr;                         // batch kernel state (grows with n)
+  BatchTable btab;                                // k_batch task table (device, cached)
   cudaEvent_t bev[2] = {nullptr, nullptr};        // kernel_timing around k_batch
   bool batch_timed = false;
   size_t bstate_cap = 0;
@@ -257,7 +258,7 @@ int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
     }
   }
   int rc = launch_batch(g, p->tl[0], p->bs, x, n, p->bstate, p->bstate_cap, fa, p->mode, p->eb,
-                        p->d_res, p->sm_count, G, p->lag_t, st, p->timing ? p->bev : nullptr);
+                        p->d_res, p->sm_count, G, p->lag_t, &p->btab, st, p->timing ? p->bev : nullptr);
   if (rc) return cuda_fail(cudaGetLastError(), "k_batch launch");
   p->launches += 1;
   p->batch_timed = p->timing;
@@ -708,6 +709,7 @@ void sel_plan_destroy(sel_plan_t p) {
   for (auto e : p->ev_k3) cudaEventDestroy(e);
   if (p->d_params) cudaFree(p->d_params);
   if (p->bstate) cudaFree(p->bstate);
+  if (p->btab.d) cudaFree(p->btab.d);
   for (auto e : p->bev)
     if (e) cudaEventDestroy(e);
   for (auto &s : p->tslots)

@@ -32,7 +32,13 @@ constexpr int kRing = 3;                       // histogram / partial buffers (f
 // addresses for cp.reduce.async.bulk; stride 65,540 words keeps every ring slot aligned.
 constexpr int kH32Stride = kNSlots + 4;
 #ifndef SEL_RWARPS
-#define SEL_RWARPS 64                          // range chunk split over min(this, CW) warps
+#define SEL_RWARPS 6                           // range chunk split over min(this, CW) warps (rotating)
+#endif
+#ifndef SEL_NO_PF
+#define SEL_NO_PF 0                            // developer probe: no L2 prefetch at claim time
+#endif
+#ifndef SEL_CLAIM
+#define SEL_CLAIM 1                            // producer: task ids claimed per atomic
 #endif
 #ifndef SEL_BATCH_PROF
 #define SEL_BATCH_PROF 0                       // 1: per-CTA cycle counters (sel_dev_batch_profile)
@@ -56,6 +62,27 @@ __device__ __forceinline__ float key_float(unsigned int k) {
 }
 struct FPart { double acc, err; unsigned long long bits, ovf; };
 
+// Division by a launch constant without a division instruction sequence (the producer
+// decodes every task on one thread; 64-bit divisions there cost ~2,400 cycles per task
+// and made the producer the critical path): q = (x * m) >> s, exact for x < 2^31 with
+// s = 31 + ceil(log2 d), m = floor(2^s / d) + 1 (x (m d - 2^s) <= x d < 2^s).
+struct FastDiv {
+  uint64_t m;
+  uint32_t s, d;
+};
+static inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t c = 0;
+  while ((1ull << c) < d) ++c;
+  FastDiv f;
+  f.d = d;
+  f.s = 31 + c;
+  f.m = ((1ull << f.s) / d) + 1;
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv &f) {
+  return (uint32_t)(((uint64_t)x * f.m) >> f.s);
+}
+
 struct BatchArgs {
   const CUtensorMap *tmaps;       // [nf], 64-B aligned, global
   const float *const *xs;         // [nf] device pointers
@@ -65,6 +92,8 @@ struct BatchArgs {
   int sampled;                    // T tasks are sampled-block tasks (no TMA tile)
   int64_t N;
   int nR, nT, phase;              // tasks per field (F: kFinTasks); phase = kFinTasks + nR + nT
+  FastDiv div_phase, div_rt, div_ntk, div_ntj;   // by phase, nR + nT, tg.ntk, tg.ntj
+  const uint4 *ttab;              // decoded task sequences of all groups (host-built)
   int rchunk;                     // floats per R task
   FinalizeArgs fa;
   int mode;
@@ -109,38 +138,55 @@ __device__ __forceinline__ int ring(const BatchArgs &a, int f) {
 
 __device__ __forceinline__ void decode(const BatchArgs &a, int nfl, long long tau, int &kind, int &f,
                                        int &id, int &phase) {
-  // phases 0 .. a.lagF-1 are the ramp, a.lagF .. nfl-1 share one size, then the tail
+  // phases 0 .. a.lagF-1 are the ramp, a.lagF .. nfl-1 share one size, then the tail.
+  // 32-bit task indices (launch_batch checks the total < 2^31), divisions by launch
+  // constants through FastDiv.
   int p = 0;
-  long long m = tau;
+  uint32_t m = (uint32_t)tau;
   const int ramp_end = nfl < a.lagF ? nfl : a.lagF;
   for (; p < ramp_end; ++p) {
-    const long long sz = phase_size(a, nfl, p);
+    const uint32_t sz = (uint32_t)phase_size(a, nfl, p);
     if (m < sz) break;
     m -= sz;
   }
+  bool full = false;              // a phase with F, R and T tasks (the common case)
   if (p == ramp_end) {
     const int nmid = nfl > a.lagF ? nfl - a.lagF : 0;
-    const long long S = (long long)kFinTasks + a.nR + a.nT;
-    if (nmid > 0 && m < nmid * S) {
-      const int q = (int)(m / S);
-      p = a.lagF + q;
-      m -= (long long)q * S;
+    const uint32_t S = (uint32_t)a.phase;
+    if (nmid > 0 && m < (uint32_t)nmid * S) {
+      const uint32_t q = fdiv(m, a.div_phase);
+      p = a.lagF + (int)q;
+      m -= q * S;
+      full = true;
     } else {
-      m -= (long long)nmid * S;
+      m -= (uint32_t)nmid * S;
       p = ramp_end + nmid;
-      while (m >= phase_size(a, nfl, p)) { m -= phase_size(a, nfl, p); ++p; }
+      while (m >= (uint32_t)phase_size(a, nfl, p)) { m -= (uint32_t)phase_size(a, nfl, p); ++p; }
     }
   }
   phase = p;
   const int nF = in_range(nfl, p - a.lagF) ? kFinTasks : 0;
-  if (m < nF) {
+  if (m < (uint32_t)nF) {
     kind = KIND_F; f = p - a.lagF; id = (int)m;
     return;
   }
   m -= nF;
-  const long long nRp = in_range(nfl, p) ? a.nR : 0, nTp = in_range(nfl, p - a.lagT) ? a.nT : 0;
-  const long long M = nRp + nTp;
-  const long long r0 = m * nRp / M, r1 = (m + 1) * nRp / M;
+  const uint32_t nRp = in_range(nfl, p) ? a.nR : 0, nTp = in_range(nfl, p - a.lagT) ? a.nT : 0;
+  const uint32_t M = nRp + nTp;
+  // Bresenham interleave of the phase's R and T tasks: r0 = floor(m nR / M)
+  uint32_t r0, r1;
+  if (full) {                     // M = nR + nT: exact quotient from a double estimate
+    const uint64_t num0 = (uint64_t)m * nRp, num1 = num0 + nRp;
+    uint32_t q0 = (uint32_t)((double)num0 / (double)M);
+    while ((uint64_t)q0 * M > num0) --q0;
+    while ((uint64_t)(q0 + 1) * M <= num0) ++q0;
+    uint32_t q1 = q0;
+    while ((uint64_t)(q1 + 1) * M <= num1) ++q1;
+    r0 = q0; r1 = q1;
+  } else {
+    r0 = (uint32_t)((uint64_t)m * nRp / M);
+    r1 = (uint32_t)(((uint64_t)m + 1) * nRp / M);
+  }
   if (r1 > r0) { kind = KIND_R; f = p; id = (int)r0; }
   else { kind = KIND_T; f = p - a.lagT; id = (int)(m - r0); }
 }
@@ -269,6 +315,8 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   const int grp = (int)(blockIdx.x % (unsigned)a.G);
   const int nfl = (a.nf - grp + a.G - 1) / a.G;                  // this group's fields
   const long long ntot = (long long)nfl * (a.nR + a.nT + kFinTasks);
+  // this group's task table: groups before it hold (fields with f % G < grp) sequences
+  const uint4 *const ttab = a.ttab + (long long)a.phase * ((long long)grp * (a.nf / a.G) + min(grp, a.nf % a.G));
   if (tid == 0) {
     s_qhead = 0u;
     s_qtail = 0u;
@@ -299,37 +347,64 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       // earlier stages are consumed; the claim's atomic itself is issued one iteration
       // before its result is needed.
       struct Dec { int kind, f, id, phase, btk, btj, bi, slot; };
-      auto decode_pf = [&](long long tau, Dec &d) {
+      // A task is decoded from one task-table entry (instead of decoding the sequence
+      // on this issue-starved thread); the entry is fetched one task before it is decoded
+      auto fetch = [&](long long tau) -> uint4 {
+        return tau < ntot ? __ldg(ttab + tau) : make_uint4(0u, 0u, 0u, 0u);
+      };
+      auto decode_pf = [&](long long tau, const uint4 e, Dec &d) {
         d.kind = KIND_NONE; d.f = 0; d.id = 0; d.phase = 0; d.btk = d.btj = d.bi = 0; d.slot = 0;
         if (tau >= ntot) { d.kind = -1; return; }
-        decode(a, nfl, tau, d.kind, d.f, d.id, d.phase);
+        d.kind = (int)(e.x & 3u);
+        d.phase = (int)(e.x >> 2);
+        d.id = (int)e.y;
+        d.f = d.phase - (d.kind == KIND_R ? 0 : d.kind == KIND_T ? a.lagT : a.lagF);
         d.slot = grp * kRing + d.f % kRing;  // = ring(a, global field)
         d.f = d.f * a.G + grp;             // global field index
         if (d.kind == KIND_T && !a.sampled) {
-          d.btk = d.id % a.tg.ntk;
-          const int rest = d.id / a.tg.ntk;
-          d.btj = rest % a.tg.ntj;
-          d.bi = rest / a.tg.ntj;
-          if constexpr (D == 3)
-            tma_prefetch_3d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1, 4 * d.bi - 1);
-          else
-            tma_prefetch_2d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1);
+          d.btk = (int)(e.z & 0xffffu);
+          d.btj = (int)(e.z >> 16);
+          d.bi = (int)e.w;
+          if (!SEL_NO_PF) {
+            if constexpr (D == 3)
+              tma_prefetch_3d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1, 4 * d.bi - 1);
+            else
+              tma_prefetch_2d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1);
+          }
         } else if (d.kind == KIND_R) {
           const long long lo = (long long)d.id * a.rchunk;
           const long long cnt = min((long long)a.rchunk, a.N - lo);
-          bulk_prefetch(a.xs[d.f] + lo, (uint32_t)(cnt * 4), pol_keep);
+          if (!SEL_NO_PF) bulk_prefetch(a.xs[d.f] + lo, (uint32_t)(cnt * 4), pol_keep);
         }
       };
+      // Tasks are claimed SEL_CLAIM consecutive ids per atomic, the next batch's atomic
+      // one batch ahead: the claim's round trip to L2 (a counter shared by the group's
+      // CTAs) is off the producer's critical path (it was ~2,000 cycles per task).
+      constexpr unsigned int K = SEL_CLAIM;
+      long long cb = (long long)atomicAdd(a.task_ctr + grp, K);
+      long long nb = cb < ntot ? (long long)atomicAdd(a.task_ctr + grp, K) : ntot;
+      unsigned int ck = 0;
+      auto next_tau = [&]() -> long long {
+        if (ck == K) {
+          cb = nb;
+          ck = 0;
+          nb = cb < ntot ? (long long)atomicAdd(a.task_ctr + grp, K) : ntot;
+        }
+        const long long t = cb + ck++;
+        return t < ntot ? t : ntot;
+      };
       Dec t0, t1;
-      long long r = (long long)atomicAdd(a.task_ctr + grp, 1u);
-      decode_pf(r, t0);
-      bool more = r < ntot;
-      r = more ? (long long)atomicAdd(a.task_ctr + grp, 1u) : ntot;
-      decode_pf(r, t1);
-      more = more && r < ntot;
-      r = more ? (long long)atomicAdd(a.task_ctr + grp, 1u) : ntot;
+      long long tau_n = next_tau();
+      decode_pf(tau_n, fetch(tau_n), t0);
+      tau_n = next_tau();
+      decode_pf(tau_n, fetch(tau_n), t1);
+      tau_n = t1.kind < 0 ? ntot : next_tau();
+      uint4 e_n = fetch(tau_n);          // in flight: the task after t1
+      long long pp_start = PCLOCK(), pp_wait = 0, pp_dec = 0, pp_n = 0;
       for (;;) {
+        const long long pw0 = PCLOCK();
         mbar_wait_sleep(&empty_bar[stage], ph ^ 1u);
+        PROF(pp_wait += clock64() - pw0; ++pp_n);
         stage_desc[stage] = make_int4(t0.kind, t0.f, t0.id, t0.phase);
         stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, t0.slot);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
@@ -356,10 +431,20 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
         if (t0.kind < 0) break;            // the sentinel went out: done
         t0 = t1;
-        decode_pf(r, t1);
-        more = more && r < ntot;
-        r = more ? (long long)atomicAdd(a.task_ctr + grp, 1u) : ntot;
+        const long long pd0 = PCLOCK();
+        decode_pf(tau_n, e_n, t1);
+        tau_n = t1.kind < 0 ? ntot : next_tau();
+        e_n = fetch(tau_n);
+        PROF(pp_dec += clock64() - pd0);
       }
+#if SEL_BATCH_PROF
+      if (a.prof) {
+        atomicAdd(a.prof + 148 * 8 + 8, (unsigned long long)(clock64() - pp_start));
+        atomicAdd(a.prof + 148 * 8 + 9, (unsigned long long)pp_wait);
+        atomicAdd(a.prof + 148 * 8 + 10, (unsigned long long)pp_dec);
+        atomicAdd(a.prof + 148 * 8 + 11, (unsigned long long)pp_n);
+      }
+#endif
     }
     return;
   }
@@ -755,10 +840,39 @@ size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G) {
          8192;
 }
 
+// The task sequence of one CTA group with nfl fields, decoded (the order the device's
+// decode() defines): phase p = F(p - lagF) [kFinTasks] then R(p) [nR] and T(p - lagT) [nT]
+// interleaved (Bresenham).  Entry: {kind | phase << 2, id, btk | btj << 16, bi}.
+static void build_group_sequence(int nfl, int nR, int nT, int lagT, int lagF, const TileGeo &tg,
+                                 bool sampled, std::vector<uint4> &out) {
+  auto inr = [&](int f) { return f >= 0 && f < nfl; };
+  for (int p = 0; p < nfl + lagF; ++p) {
+    if (inr(p - lagF))
+      for (int k = 0; k < kFinTasks; ++k) out.push_back(make_uint4(KIND_F | (uint32_t)p << 2, (uint32_t)k, 0u, 0u));
+    const long long nRp = inr(p) ? nR : 0, nTp = inr(p - lagT) ? nT : 0, M = nRp + nTp;
+    for (long long m = 0; m < M; ++m) {
+      const long long r0 = m * nRp / M, r1 = (m + 1) * nRp / M;
+      if (r1 > r0) {
+        out.push_back(make_uint4(KIND_R | (uint32_t)p << 2, (uint32_t)r0, 0u, 0u));
+      } else {
+        const int id = (int)(m - r0);
+        uint32_t z = 0, w = 0;
+        if (!sampled && tg.ntk > 0 && tg.ntj > 0) {
+          const int btk = id % tg.ntk, rest = id / tg.ntk;
+          z = (uint32_t)btk | (uint32_t)(rest % tg.ntj) << 16;
+          w = (uint32_t)(rest / tg.ntj);
+        }
+        out.push_back(make_uint4(KIND_T | (uint32_t)p << 2, (uint32_t)id, z, w));
+      }
+    }
+  }
+}
+
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
-                 sel_result *d_results, int sm_count, int G, int lagT, cudaStream_t st,
+                 sel_result *d_results, int sm_count, int G, int lagT, BatchTable *tab, cudaStream_t st,
                  cudaEvent_t *ev) {
+  if (!tab || tl.tg.ntk >= (1 << 16) || tl.tg.ntj >= (1 << 16)) return SEL_EINVAL;
   if (G < 1 || G > nf || G > sm_count || lagT < 1 || lagT > 4) return SEL_EINVAL;
   // state layout (device): tmaps | xs | params | counters | hist x2 | tpart x2 | fpart x2
   char *b = (char *)state;
@@ -807,6 +921,32 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   a.nR = bs.nR;
   a.nT = nT;
   a.phase = kFinTasks + bs.nR + nT;
+  if ((long long)nf * a.phase >= (1LL << 31)) return SEL_EINVAL;   // 32-bit task indices
+  {   // task table, rebuilt only when its key changes
+    const long long key[8] = {nf, G, bs.nR, nT, lagT, sampled ? 1 : 0, tl.tg.ntk, tl.tg.ntj};
+    if (memcmp(key, tab->key, sizeof(key)) != 0) {
+      static thread_local std::vector<uint4> h;
+      h.clear();
+      h.reserve((size_t)nf * a.phase);
+      for (int gi = 0; gi < G; ++gi)
+        build_group_sequence((nf - gi + G - 1) / G, bs.nR, nT, lagT, lagT + 2, tl.tg, sampled, h);
+      const size_t bytes = h.size() * sizeof(uint4);
+      if (bytes > tab->cap) {
+        if (tab->d) { cudaStreamSynchronize(st); cudaFree(tab->d); }
+        tab->d = nullptr;
+        tab->cap = 0;
+        if (cudaMalloc(&tab->d, bytes) != cudaSuccess) return SEL_ENOMEM;
+        tab->cap = bytes;
+      }
+      if (cudaMemcpyAsync(tab->d, h.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) return SEL_ECUDA;
+      memcpy(tab->key, key, sizeof(key));
+    }
+  }
+  a.ttab = (const uint4 *)tab->d;
+  a.div_phase = make_fastdiv((uint32_t)a.phase);
+  a.div_rt = make_fastdiv((uint32_t)(bs.nR + nT));
+  a.div_ntk = make_fastdiv((uint32_t)(tl.tg.ntk > 0 ? tl.tg.ntk : 1));
+  a.div_ntj = make_fastdiv((uint32_t)(tl.tg.ntj > 0 ? tl.tg.ntj : 1));
   a.rchunk = bs.rchunk;
   a.fa = fa;
   a.mode = mode;

@@ -131,14 +131,22 @@ struct BatchSizes {
   int cw;           // consumer warps
 };
 
+// k_batch task table: the decoded task sequence of every CTA group (uint4 per task), built
+// on the host and cached on the device per (fields, groups, task counts) key
+struct BatchTable {
+  void *d = nullptr;
+  size_t cap = 0;
+  long long key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+};
+
 bool tile_supported(const Geo &g);
 int batch_sizes(const Geo &g, BatchSizes *bs);
 size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G);
 int batch_ntasks(const Geo &g, const TileLaunch &tl, const BatchSizes &bs);
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
-                 sel_result *d_results, int sm_count, int G, int lagT, cudaStream_t st,
-                 cudaEvent_t *ev);
+                 sel_result *d_results, int sm_count, int G, int lagT, BatchTable *tab,
+                 cudaStream_t st, cudaEvent_t *ev);
 int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl);
 int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Workspace &ws,
                 const DebugPtrs *dbg, cudaStream_t st);

@@ -51,7 +51,7 @@ for row in rows:
     print("field", *row)
 # k_batch per-phase cycle breakdown (warp 0 of each CTA)
 import ctypes
-buf = torch.zeros(148 * 8 + 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(148 * 8 + 16, dtype=torch.int64, device="cuda")
 sel.lib().sel_dev_batch_profile(ctypes.c_void_p(buf.data_ptr()))
 p.set_option("kernel_timing", 0)
 p.estimate_batch(fields)
@@ -65,4 +65,7 @@ tot = v[:, :6].sum(1)
 print("k_batch warp-0 cycles per CTA (mean):", {n: f"{v[:, k].mean()/1e3:.1f}k ({v[:, k].mean()/tot.mean()*100:.0f}%)" for k, n in enumerate(names)})
 print("flushes per CTA %.1f, publishes per warp0 %.1f" % (v[:, 6].mean(), v[:, 7].mean()))
 print("CTA total spread: min %.1fk max %.1fk" % (tot.min()/1e3, tot.max()/1e3))
+pr = buf[148 * 8 + 8:148 * 8 + 12].double().cpu().numpy() / 148
+print("producer per CTA: total %.1fk, empty-wait %.1fk, decode %.1fk, tasks %.0f -> %.0f cycles/task decode, %.0f cycles/task total"
+      % (pr[0] / 1e3, pr[1] / 1e3, pr[2] / 1e3, pr[3], pr[2] / max(pr[3], 1), pr[0] / max(pr[3], 1)))
 sel.lib().sel_dev_batch_profile(None)
