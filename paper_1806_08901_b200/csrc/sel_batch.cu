@@ -367,9 +367,9 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
           d.bi = (int)e.w;
           if (!SEL_NO_PF) {
             if constexpr (D == 3)
-              tma_prefetch_3d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1, 4 * d.bi - 1);
+              tma_prefetch_3d(a.tmaps + d.f, 128 * d.btk - 4, 4 * Cfg::ROWS * d.btj - 1, 4 * d.bi - 1);
             else
-              tma_prefetch_2d(a.tmaps + d.f, 128 * d.btk - 4, 4 * CW * d.btj - 1);
+              tma_prefetch_2d(a.tmaps + d.f, 128 * d.btk - 4, 4 * Cfg::ROWS * d.btj - 1);
           }
         } else if (d.kind == KIND_R) {
           const long long lo = (long long)d.id * a.rchunk;
@@ -415,10 +415,10 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         } else if (t0.kind == KIND_T && !a.sampled) {
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
-            tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
+            tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * Cfg::ROWS * t0.btj - 1,
                              4 * t0.bi - 1, &full_bar[stage], pol_last);
           else
-            tma_load_2d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * CW * t0.btj - 1,
+            tma_load_2d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * Cfg::ROWS * t0.btj - 1,
                              &full_bar[stage], pol_last);
         } else if (t0.kind == KIND_R) {
           const long long lo = (long long)t0.id * a.rchunk;

@@ -73,15 +73,15 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
         if constexpr (Cfg::DIRECT) {     // descriptor only; the tile box goes to L2
           asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
                            reinterpret_cast<uint64_t>(&tmap)),
-                       "r"(128 * btk - 4), "r"(4 * CW * btj - 1), "r"(4 * bi - 1)
+                       "r"(128 * btk - 4), "r"(4 * Cfg::ROWS * btj - 1), "r"(4 * bi - 1)
                        : "memory");
           mbar_arrive(&full_bar[stage]);
         } else {
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
-            tma_load_3d(dst, &tmap, 128 * btk - 4, 4 * CW * btj - 1, 4 * bi - 1, &full_bar[stage]);
+            tma_load_3d(dst, &tmap, 128 * btk - 4, 4 * Cfg::ROWS * btj - 1, 4 * bi - 1, &full_bar[stage]);
           else
-            tma_load_2d(dst, &tmap, 128 * btk - 4, 4 * CW * btj - 1, &full_bar[stage]);
+            tma_load_2d(dst, &tmap, 128 * btk - 4, 4 * Cfg::ROWS * btj - 1, &full_bar[stage]);
         }
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
       }
@@ -153,8 +153,9 @@ bool tile_supported(const Geo &g) {
 int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl) {
   TileGeo &t = tl->tg;
   const int cw = g.ndims == 3 ? TileCfg<3>::CW : TileCfg<2>::CW;
+  const int rows = g.ndims == 3 ? TileCfg<3>::ROWS : TileCfg<2>::ROWS;   // block rows per tile
   for (int a = 0; a < 3; ++a) { t.n[a] = g.n[a]; t.nb[a] = (int)g.nb[a]; }
-  t.ntj = (int)((g.nb[1] + cw - 1) / cw);
+  t.ntj = (int)((g.nb[1] + rows - 1) / rows);
   t.ntk = (int)((g.nb[2] + 31) / 32);
   const int64_t nt = (int64_t)t.ntj * t.ntk * (g.ndims == 3 ? g.nb[0] : 1);
   if (nt > (1LL << 26)) return SEL_EINVAL;

@@ -12,16 +12,19 @@ namespace sel {
 
 // tile configuration (developer overrides for sweeps: -DSEL_CW2=... etc.)
 #ifndef SEL_CW2
-#define SEL_CW2 24
+#define SEL_CW2 22
 #endif
 #ifndef SEL_STAGES2
-#define SEL_STAGES2 3
+#define SEL_STAGES2 2
 #endif
 #ifndef SEL_W2
 #define SEL_W2 8192            // shared-memory histogram window (bins), 2D
 #endif
 #ifndef SEL_W3
 #define SEL_W3 12288           // 3D
+#endif
+#ifndef SEL_BR2
+#define SEL_BR2 2              // 2D: block rows per consumer warp and tile task
 #endif
 #ifndef SEL_DIRECT3
 #define SEL_DIRECT3 0          // 1: 3D tiles read straight from L2 into registers (no smem stage)
@@ -48,7 +51,9 @@ struct TileCfg {
   static constexpr bool DIRECT = D == 3 && SEL_DIRECT3;
   static constexpr int CW = D == 3 ? SEL_CW3 : SEL_CW2;           // consumer warps
   static constexpr int THREADS = (CW + 1) * 32;
-  static constexpr int BOXJ = 4 * CW + 1;                         // halo row + 4 per warp
+  static constexpr int BR = D == 2 ? SEL_BR2 : 1;                 // block rows per warp
+  static constexpr int ROWS = CW * BR;                            // block rows per tile
+  static constexpr int BOXJ = 4 * ROWS + 1;                       // halo row + 4 per block row
   static constexpr int BOXI = D == 3 ? 5 : 1;                     // halo plane + 4 (3D)
   static constexpr int PLANE = kBoxK * BOXJ;                      // floats per smem plane
   static constexpr uint32_t STAGE_BYTES = PLANE * BOXI * 4;
@@ -202,20 +207,22 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
                                              unsigned int &ovf, const DebugPtrs &dbg,
                                              uint64_t &tbits, double &terr) {
   using Cfg = TileCfg<D>;
-  constexpr int CW = Cfg::CW;
   constexpr int SZ = Tab<D>::SIZE;
   constexpr int NPL = D == 3 ? 4 : 1;
   // per-axis extents and block coordinates fit 32 bits (tile_supported); only the debug
   // dumps form 64-bit linear indices
   const int n0 = (int)tg.n[0], n1 = (int)tg.n[1], n2 = (int)tg.n[2];
-    const int bj = btj * CW + warp;
-    const int bk = btk * 32 + lane;
-    tbits = 0;
-    terr = 0.0;
+  const int bk = btk * 32 + lane;
+  tbits = 0;
+  terr = 0.0;
+#pragma unroll 1
+  for (int rb = 0; rb < Cfg::BR; ++rb) {          // the warp's block rows, in order
+    const int wr = warp * Cfg::BR + rb;           // block row within the tile
+    const int bj = btj * Cfg::ROWS + wr;
     if (ok && bj < tg.nb[1]) {
       const bool activeK = bk < tg.nb[2];
       const int I0 = 4 * bi, J0 = 4 * bj, K0 = 4 * bk;
-      const float *wrow = S + (4 * warp) * kBoxK;   // smem row of j = J0 - 1 (plane 0)
+      const float *wrow = S + (4 * wr) * kBoxK;     // smem row of j = J0 - 1 (plane 0)
       const float rf = lane_rf(activeK, r_f);
       // ---------------- SZ: nested differences on the tile (R4), codes -> histogram (R5)
       float dprev[4][4];
@@ -315,7 +322,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
             for (int r = 0; r < 4; ++r) {
               const int jc = min(J0 + r, n1 - 1) - J0;         // 0..3
               const float4 q = *reinterpret_cast<const float4 *>(
-                  pbase + (4 * warp + 1 + jc) * kBoxK + 4 + 4 * lane);
+                  pbase + (4 * wr + 1 + jc) * kBoxK + 4 + 4 * lane);
               const int o = (p * 4 + r) * 4;
               blk[o] = q.x; blk[o + 1] = q.y; blk[o + 2] = q.z; blk[o + 3] = q.w;
             }
@@ -327,8 +334,8 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
         int cf[SZ];
         uint32_t u[SZ];
         zfp_block<D, DBG>(blk, minexp, bits, E, emax, cf, u);
-        tbits = bits;
-        terr = E;
+        tbits += bits;
+        terr += E;
         if constexpr (DBG) {
           const int64_t tb = (D == 3 ? ((int64_t)bi * tg.nb[1] + bj) : (int64_t)bj) * tg.nb[2] + bk;   // block index
           dbg.emax[tb] = emax; dbg.bits[tb] = bits; dbg.err[tb] = E;
@@ -337,6 +344,7 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
         }
       }
     }
+  }
 }
 
 // Direct 3D tile task (TileCfg<3>::DIRECT): same work and results as tile_consume, but
