@@ -62,27 +62,6 @@ __device__ __forceinline__ float key_float(unsigned int k) {
 }
 struct FPart { double acc, err; unsigned long long bits, ovf; };
 
-// Division by a launch constant without a division instruction sequence (the producer
-// decodes every task on one thread; 64-bit divisions there cost ~2,400 cycles per task
-// and made the producer the critical path): q = (x * m) >> s, exact for x < 2^31 with
-// s = 31 + ceil(log2 d), m = floor(2^s / d) + 1 (x (m d - 2^s) <= x d < 2^s).
-struct FastDiv {
-  uint64_t m;
-  uint32_t s, d;
-};
-static inline FastDiv make_fastdiv(uint32_t d) {
-  uint32_t c = 0;
-  while ((1ull << c) < d) ++c;
-  FastDiv f;
-  f.d = d;
-  f.s = 31 + c;
-  f.m = ((1ull << f.s) / d) + 1;
-  return f;
-}
-__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv &f) {
-  return (uint32_t)(((uint64_t)x * f.m) >> f.s);
-}
-
 struct BatchArgs {
   const CUtensorMap *tmaps;       // [nf], 64-B aligned, global
   const float *const *xs;         // [nf] device pointers
@@ -92,7 +71,6 @@ struct BatchArgs {
   int sampled;                    // T tasks are sampled-block tasks (no TMA tile)
   int64_t N;
   int nR, nT, phase;              // tasks per field (F: kFinTasks); phase = kFinTasks + nR + nT
-  FastDiv div_phase, div_rt, div_ntk, div_ntj;   // by phase, nR + nT, tg.ntk, tg.ntj
   const uint4 *ttab;              // decoded task sequences of all groups (host-built)
   int rchunk;                     // floats per R task
   FinalizeArgs fa;
@@ -134,61 +112,6 @@ __device__ __forceinline__ long long phase_size(const BatchArgs &a, int nfl, int
 // buffer slot of field f: kRing per group, reused by field f + kRing * G
 __device__ __forceinline__ int ring(const BatchArgs &a, int f) {
   return (f % a.G) * kRing + (f / a.G) % kRing;
-}
-
-__device__ __forceinline__ void decode(const BatchArgs &a, int nfl, long long tau, int &kind, int &f,
-                                       int &id, int &phase) {
-  // phases 0 .. a.lagF-1 are the ramp, a.lagF .. nfl-1 share one size, then the tail.
-  // 32-bit task indices (launch_batch checks the total < 2^31), divisions by launch
-  // constants through FastDiv.
-  int p = 0;
-  uint32_t m = (uint32_t)tau;
-  const int ramp_end = nfl < a.lagF ? nfl : a.lagF;
-  for (; p < ramp_end; ++p) {
-    const uint32_t sz = (uint32_t)phase_size(a, nfl, p);
-    if (m < sz) break;
-    m -= sz;
-  }
-  bool full = false;              // a phase with F, R and T tasks (the common case)
-  if (p == ramp_end) {
-    const int nmid = nfl > a.lagF ? nfl - a.lagF : 0;
-    const uint32_t S = (uint32_t)a.phase;
-    if (nmid > 0 && m < (uint32_t)nmid * S) {
-      const uint32_t q = fdiv(m, a.div_phase);
-      p = a.lagF + (int)q;
-      m -= q * S;
-      full = true;
-    } else {
-      m -= (uint32_t)nmid * S;
-      p = ramp_end + nmid;
-      while (m >= (uint32_t)phase_size(a, nfl, p)) { m -= (uint32_t)phase_size(a, nfl, p); ++p; }
-    }
-  }
-  phase = p;
-  const int nF = in_range(nfl, p - a.lagF) ? kFinTasks : 0;
-  if (m < (uint32_t)nF) {
-    kind = KIND_F; f = p - a.lagF; id = (int)m;
-    return;
-  }
-  m -= nF;
-  const uint32_t nRp = in_range(nfl, p) ? a.nR : 0, nTp = in_range(nfl, p - a.lagT) ? a.nT : 0;
-  const uint32_t M = nRp + nTp;
-  // Bresenham interleave of the phase's R and T tasks: r0 = floor(m nR / M)
-  uint32_t r0, r1;
-  if (full) {                     // M = nR + nT: exact quotient from a double estimate
-    const uint64_t num0 = (uint64_t)m * nRp, num1 = num0 + nRp;
-    uint32_t q0 = (uint32_t)((double)num0 / (double)M);
-    while ((uint64_t)q0 * M > num0) --q0;
-    while ((uint64_t)(q0 + 1) * M <= num0) ++q0;
-    uint32_t q1 = q0;
-    while ((uint64_t)(q1 + 1) * M <= num1) ++q1;
-    r0 = q0; r1 = q1;
-  } else {
-    r0 = (uint32_t)((uint64_t)m * nRp / M);
-    r1 = (uint32_t)(((uint64_t)m + 1) * nRp / M);
-  }
-  if (r1 > r0) { kind = KIND_R; f = p; id = (int)r0; }
-  else { kind = KIND_T; f = p - a.lagT; id = (int)(m - r0); }
 }
 
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
@@ -408,11 +331,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         stage_desc[stage] = make_int4(t0.kind, t0.f, t0.id, t0.phase);
         stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, t0.slot);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
-        if (Cfg::DIRECT && t0.kind == KIND_T) {
-          // direct tiles: no staged data, the consumers read the box from L2 (prefetched
-          // when the task was claimed)
-          mbar_arrive(&full_bar[stage]);
-        } else if (t0.kind == KIND_T && !a.sampled) {
+        if (t0.kind == KIND_T && !a.sampled) {
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           if constexpr (D == 3)
             tma_load_3d_hint(dst, a.tmaps + t0.f, 128 * t0.btk - 4, 4 * Cfg::ROWS * t0.btj - 1,
@@ -637,10 +556,6 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
 
     if (kind == KIND_T) {
       const int4 tc = stage_tile[stage];
-      if constexpr (Cfg::DIRECT) {   // descriptor read: the slot is free again
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[stage]);
-      }
       if (cur < 0) {               // first tile of field f here: params, ring slot free
         // per warp (no CTA barrier): lane 0 acquires the flags, the warp barrier orders
         // the lanes' L2 reads (ld.cg: never a stale L1 line) after it
@@ -662,19 +577,14 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         sampled_consume<D>(a.xs[f], a.g, t, ok && t < a.g.n_pb, r_f, minexp, hist,
                            a.hist + (size_t)tc.w * kH32Stride + 1, ovf, tbits,
                            terr);
-      } else if constexpr (Cfg::DIRECT) {
-        tile_consume_direct<false>(a.xs[f], tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hist,
-                                   a.hist + (size_t)tc.w * kH32Stride + 1, ovf, nodbg, tbits, terr);
       } else {
         tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hist,
                                a.hist + (size_t)tc.w * kH32Stride + 1, ovf,
                                nodbg, tbits, terr);
       }
       ++cur_tasks;
-      if constexpr (!Cfg::DIRECT) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[stage]);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[stage]);
       task_store(a.tpart + (size_t)tc.w * a.nT * CW, id * CW + warp, tbits, terr);
     } else if (kind == KIND_R) {
       // ---- min / max / non-finite of the staged chunk (R1) by kRWarps consumer warps
@@ -840,8 +750,7 @@ size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G) {
          8192;
 }
 
-// The task sequence of one CTA group with nfl fields, decoded (the order the device's
-// decode() defines): phase p = F(p - lagF) [kFinTasks] then R(p) [nR] and T(p - lagT) [nT]
+// The task sequence of one CTA group with nfl fields, decoded: phase p = F(p - lagF) [kFinTasks] then R(p) [nR] and T(p - lagT) [nT]
 // interleaved (Bresenham).  Entry: {kind | phase << 2, id, btk | btj << 16, bi}.
 static void build_group_sequence(int nfl, int nR, int nT, int lagT, int lagF, const TileGeo &tg,
                                  bool sampled, std::vector<uint4> &out) {
@@ -943,10 +852,6 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
     }
   }
   a.ttab = (const uint4 *)tab->d;
-  a.div_phase = make_fastdiv((uint32_t)a.phase);
-  a.div_rt = make_fastdiv((uint32_t)(bs.nR + nT));
-  a.div_ntk = make_fastdiv((uint32_t)(tl.tg.ntk > 0 ? tl.tg.ntk : 1));
-  a.div_ntj = make_fastdiv((uint32_t)(tl.tg.ntj > 0 ? tl.tg.ntj : 1));
   a.rchunk = bs.rchunk;
   a.fa = fa;
   a.mode = mode;

@@ -21,8 +21,7 @@ namespace sel {
 
 template <int D, bool DBG>
 __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
-    k_tile(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ x, TileGeo tg,
-           Workspace ws, DebugPtrs dbg) {
+    k_tile(const __grid_constant__ CUtensorMap tmap, TileGeo tg, Workspace ws, DebugPtrs dbg) {
   using Cfg = TileCfg<D>;
   constexpr int CW = Cfg::CW;
   extern __shared__ float smem_dyn[];
@@ -70,19 +69,11 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
         const int bi = rest / tg.ntj;
         stage_task[stage] = make_int4(t, btk, btj, bi);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
-        if constexpr (Cfg::DIRECT) {     // descriptor only; the tile box goes to L2
-          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                           reinterpret_cast<uint64_t>(&tmap)),
-                       "r"(128 * btk - 4), "r"(4 * Cfg::ROWS * btj - 1), "r"(4 * bi - 1)
-                       : "memory");
-          mbar_arrive(&full_bar[stage]);
-        } else {
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-          if constexpr (D == 3)
-            tma_load_3d(dst, &tmap, 128 * btk - 4, 4 * Cfg::ROWS * btj - 1, 4 * bi - 1, &full_bar[stage]);
-          else
-            tma_load_2d(dst, &tmap, 128 * btk - 4, 4 * Cfg::ROWS * btj - 1, &full_bar[stage]);
-        }
+        mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+        if constexpr (D == 3)
+          tma_load_3d(dst, &tmap, 128 * btk - 4, 4 * Cfg::ROWS * btj - 1, 4 * bi - 1, &full_bar[stage]);
+        else
+          tma_load_2d(dst, &tmap, 128 * btk - 4, 4 * Cfg::ROWS * btj - 1, &full_bar[stage]);
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
       }
     }
@@ -105,17 +96,10 @@ __global__ void __launch_bounds__(TileCfg<D>::THREADS, 1)
     const float *S = base + stage * Cfg::STAGE_FLOATS;
     uint64_t tbits = 0;
     double terr = 0.0;
-    if constexpr (Cfg::DIRECT) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[stage]);    // descriptor read: slot free
-      tile_consume_direct<DBG>(x, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hist, ws.hist,
-                               ovf, dbg, tbits, terr);
-    } else {
-      tile_consume<D, DBG>(S, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hist, ws.hist, ovf,
-                           dbg, tbits, terr);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[stage]);    // stage free for the producer
-    }
+    tile_consume<D, DBG>(S, td.y, td.z, td.w, tg, warp, lane, ok, r_f, minexp, hist, ws.hist, ovf,
+                         dbg, tbits, terr);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[stage]);    // stage free for the producer
     task_store(ws.task_part, t * CW + warp, tbits, terr);
     if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
   }
@@ -207,8 +191,7 @@ int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Worksp
   if (dbg) d = *dbg;
   TileGeo tg = tl.tg;
   Workspace w = ws;
-  const float *xp = x;
-  void *args[] = {(void *)&map, (void *)&xp, (void *)&tg, (void *)&w, (void *)&d};
+  void *args[] = {(void *)&map, (void *)&tg, (void *)&w, (void *)&d};
   const void *fn = rank == 3 ? tile_fn<3>(dbg != nullptr) : tile_fn<2>(dbg != nullptr);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tl.ctas);

@@ -26,17 +26,11 @@ namespace sel {
 #ifndef SEL_BR2
 #define SEL_BR2 2              // 2D: block rows per consumer warp and tile task
 #endif
-#ifndef SEL_DIRECT3
-#define SEL_DIRECT3 0          // 1: 3D tiles read straight from L2 into registers (no smem stage)
-#endif
 #ifndef SEL_CW3
-#define SEL_CW3 (SEL_DIRECT3 ? 14 : 8)
+#define SEL_CW3 8
 #endif
 #ifndef SEL_STAGES3
-#define SEL_STAGES3 (SEL_DIRECT3 ? 4 : 2)
-#endif
-#ifndef SEL_RSTAGE3
-#define SEL_RSTAGE3 8192       // direct 3D: floats per stage (range chunks only)
+#define SEL_STAGES3 2
 #endif
 
 constexpr int kBoxK = 4 * 32 + 4;             // 132 floats: 4 halo columns (last one used) + 128
@@ -44,11 +38,6 @@ constexpr int kChunk = 1024;                  // window flush granule (bins)
 
 template <int D>
 struct TileCfg {
-  // DIRECT: a tile task carries no staged data; each lane loads its block (+ halo) from
-  // global memory (L2: the producer prefetches the tile box) into registers.  Without the
-  // 2 x 87 KB smem stages of the 3D box the CTA can run as many consumer warps as the
-  // register file allows (3D is latency-bound: throughput scales with warps).
-  static constexpr bool DIRECT = D == 3 && SEL_DIRECT3;
   static constexpr int CW = D == 3 ? SEL_CW3 : SEL_CW2;           // consumer warps
   static constexpr int THREADS = (CW + 1) * 32;
   static constexpr int BR = D == 2 ? SEL_BR2 : 1;                 // block rows per warp
@@ -57,8 +46,7 @@ struct TileCfg {
   static constexpr int BOXI = D == 3 ? 5 : 1;                     // halo plane + 4 (3D)
   static constexpr int PLANE = kBoxK * BOXJ;                      // floats per smem plane
   static constexpr uint32_t STAGE_BYTES = PLANE * BOXI * 4;
-  // direct: the stages only carry range chunks (cp.async.bulk), tile tasks no data
-  static constexpr int STAGE_FLOATS = DIRECT ? SEL_RSTAGE3 : ((STAGE_BYTES + 127) & ~127) / 4;
+  static constexpr int STAGE_FLOATS = ((STAGE_BYTES + 127) & ~127) / 4;
   static constexpr int STAGES = D == 3 ? SEL_STAGES3 : SEL_STAGES2;
   // One CTA-wide histogram window of W u32 bins in shared memory, codes [-W/2, W/2),
   // one copy: smem atomic increments with unused results compile to ATOMS.POPC.INC,
@@ -343,162 +331,6 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
           for (int n = 0; n < SZ; ++n) { dbg.coef[tb * SZ + n] = cf[n]; dbg.uword[tb * SZ + n] = u[n]; }
         }
       }
-    }
-  }
-}
-
-// Direct 3D tile task (TileCfg<3>::DIRECT): same work and results as tile_consume, but
-// the lane's 4x4x4 block, the -1 halo plane / row of the warp's block row and the left
-// neighbour column come from global memory (L2) instead of a TMA-staged smem tile.  All
-// lanes of a warp share (I0, J0), so a row's left neighbour (k = K0 - 1) is the previous
-// lane's last column (SHFL); lane 0 loads it (zero at k = 0, R4).  Rows / planes past the
-// field's far edge are clamped (edge replication for ZFP, R17) and carry no SZ point.
-__device__ __forceinline__ float4 ldg4(const float *p) {
-  return __ldg(reinterpret_cast<const float4 *>(p));
-}
-
-template <bool DBG, typename GH>
-__device__ __forceinline__ void tile_consume_direct(const float *__restrict__ x, int btk, int btj,
-                                                    int bi, const TileGeo &tg, int warp, int lane,
-                                                    bool ok, float r_f, int minexp,
-                                                    unsigned int *win,
-                                                    GH *ghist, unsigned int &ovf,
-                                                    const DebugPtrs &dbg, uint64_t &tbits,
-                                                    double &terr) {
-  using Cfg = TileCfg<3>;
-  constexpr int CW = Cfg::CW;
-  const int n0 = (int)tg.n[0], n1 = (int)tg.n[1], n2 = (int)tg.n[2];
-  const int bj = btj * CW + warp;
-  const int bk0 = btk * 32 + lane;
-  tbits = 0;
-  terr = 0.0;
-  if (!ok || bj >= tg.nb[1]) return;                    // warp-uniform
-  const bool activeK = bk0 < tg.nb[2];
-  const int bk = activeK ? bk0 : tg.nb[2] - 1;          // inactive lanes: a valid block
-  const int I0 = 4 * bi, J0 = 4 * bj, K0 = 4 * bk;
-  const float rf = lane_rf(activeK, r_f);
-  auto row = [&](int i, int j) -> const float * { return x + ((int64_t)i * n1 + j) * n2; };
-  // previous lane's last column = this lane's k = K0 - 1 (lane 0: load, 0 at k = 0)
-  auto left = [&](float v3, const float *r) -> float {
-    const float s = __shfl_up_sync(0xffffffffu, v3, 1);
-    return lane == 0 ? (K0 > 0 ? __ldg(r + K0 - 1) : 0.0f) : s;
-  };
-  // the block, edge-replicated (R17)
-  float blk[64];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int ic = min(I0 + p, n0 - 1);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const float4 q = ldg4(row(ic, min(J0 + r, n1 - 1)) + K0);
-      const int o = (p * 4 + r) * 4;
-      blk[o] = q.x; blk[o + 1] = q.y; blk[o + 2] = q.z; blk[o + 3] = q.w;
-    }
-  }
-  // ---------------- SZ: nested differences (R4), codes -> histogram (R5)
-  float dprev[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) dprev[r][c] = 0.0f;
-  if (I0 > 0) {                  // plane i = I0 - 1: its D2 differences (zeros at i < 0)
-    const int i = I0 - 1;
-    float d1up[4];
-    {
-      float u[4] = {0.f, 0.f, 0.f, 0.f};
-      float hl = 0.0f;
-      if (J0 > 0) {
-        const float *rp = row(i, J0 - 1);
-        const float4 q = ldg4(rp + K0);
-        u[0] = q.x; u[1] = q.y; u[2] = q.z; u[3] = q.w;
-        hl = left(u[3], rp);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) d1up[c] = u[c] - (c ? u[c - 1] : hl);
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const float *rp = row(i, min(J0 + r, n1 - 1));
-      const float4 q = ldg4(rp + K0);
-      const float v[4] = {q.x, q.y, q.z, q.w};
-      const float hl = left(v[3], rp);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float d1 = v[c] - (c ? v[c - 1] : hl);
-        dprev[r][c] = d1 - d1up[c];
-        d1up[c] = d1;
-      }
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int i = I0 + p;
-    if (i >= n0) break;                                  // padded planes: no SZ point
-    float d1up[4];
-    {
-      float u[4] = {0.f, 0.f, 0.f, 0.f};
-      float hl = 0.0f;
-      if (J0 > 0) {
-        const float *rp = row(i, J0 - 1);
-        const float4 q = ldg4(rp + K0);
-        u[0] = q.x; u[1] = q.y; u[2] = q.z; u[3] = q.w;
-        hl = left(u[3], rp);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) d1up[c] = u[c] - (c ? u[c - 1] : hl);
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int j = J0 + r;
-      if (j >= n1) break;                                // padded rows: no SZ point
-      const float *v = blk + (p * 4 + r) * 4;
-      const float hl = left(v[3], row(i, j));
-      uint32_t w[4];
-      uint32_t any = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float d1 = v[c] - (c ? v[c - 1] : hl);
-        const float d2 = d1 - d1up[c];
-        d1up[c] = d1;
-        const float d = d2 - dprev[r][c];
-        dprev[r][c] = d2;
-        w[c] = sz_win<3>(d, rf, win);
-        any |= w[c];
-      }
-      // the field origin is stored verbatim, not coded (R4): undo its count
-      const bool orow = (i == 0) && (j == 0) && (btk == 0);
-      if (orow && lane == 0) {
-        if (w[0] < (uint32_t)Cfg::W) atomicSub(win + w[0], 1u);
-        w[0] = 0u;
-      }
-      if constexpr (DBG) {
-        if (activeK) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if (orow && lane == 0 && c == 0) continue;
-            const uint32_t sl = w[c] + (Cfg::kWOff - kSlotOff);
-            dbg.codes[((int64_t)i * n1 + j) * n2 + K0 + c] = sl > 65534u ? kOvfSlot : (int32_t)sl;
-          }
-        }
-      }
-      sz_far<3>(w, any, activeK, ghist, ovf);
-    }
-  }
-  // ---------------- ZFP on the lane's block (already edge-replicated)
-  if (activeK) {
-    uint32_t bits;
-    double E;
-    int emax;
-    int cf[64];
-    uint32_t u[64];
-    zfp_block<3, DBG>(blk, minexp, bits, E, emax, cf, u);
-    tbits = bits;
-    terr = E;
-    if constexpr (DBG) {
-      const int64_t tb = ((int64_t)bi * tg.nb[1] + bj) * tg.nb[2] + bk;
-      dbg.emax[tb] = emax; dbg.bits[tb] = bits; dbg.err[tb] = E;
-#pragma unroll
-      for (int n = 0; n < 64; ++n) { dbg.coef[tb * 64 + n] = cf[n]; dbg.uword[tb * 64 + n] = u[n]; }
     }
   }
 }

@@ -301,6 +301,25 @@ def test_batch_groups(sel, orc, groups):
         compare_scalars(out[i], orc.estimate(x, 1e-3), f"G{groups}/{i}")
 
 
+@pytest.mark.parametrize("lag", [1, 2, 4])
+def test_batch_lag_and_task_table_cache(sel, orc, lag):
+    """Range lead (lag) variants, and one plan reused for stacks of different sizes and
+    group counts: the host-built task table (cached per key) is rebuilt whenever the
+    sequence changes; every result equals the oracle's."""
+    shape = (36, 260)
+    rng = np.random.default_rng(100 + lag)
+    xs = [np.cumsum(rng.standard_normal(shape), axis=0).astype(np.float32) for _ in range(7)]
+    ts = [torch.from_numpy(x).cuda() for x in xs]
+    ref = [orc.estimate(x, 1e-3) for x in xs]
+    with sel.Plan(shape, 1e-3) as p:
+        p.set_option("lag", lag)
+        for n, g in ((7, 0), (3, 1), (7, 2), (5, 0), (7, 0)):
+            p.set_option("groups", g)
+            out = p.estimate_batch(ts[:n])
+            for i in range(n):
+                compare_scalars(out[i], ref[i], f"lag{lag}/n{n}/G{g}/{i}")
+
+
 @pytest.mark.parametrize("where", ["pinned", "cuda"])
 @pytest.mark.parametrize("batch_kernel", [1, 0])
 def test_estimate_batch_async(sel, orc, where, batch_kernel):
