@@ -214,9 +214,9 @@ bool batch_ok(sel_plan_t p, const float *const *x, int n) {
 // their tiles (kLagT per group) must stay in L2 (~126 MB), hence the byte budget.
 int batch_groups(sel_plan_t p, int n) {
   int G = p->groups;
-  if (G <= 0) {                   // measured: ~80 MB of fields in flight
-    const double fb = (double)p->geo.N * 4.0;
-    G = (int)(80e6 / fb);
+  if (G <= 0) {                   // measured: ~160 MB of fields per
+    const double fb = (double)p->geo.N * 4.0;   // group sequence (C2: G = 6; 100 MB C3: 1)
+    G = (int)(160e6 / fb);
     // sampled strides: little tile work per field, so the per-field pipeline latency
     // dominates -- more groups in flight (C2 at stride (1,10): G 3 -> 10, +42%)
     if (p->sampled_ok && G < 16) G = 16;

@@ -14,6 +14,8 @@ for cfg, nf in (((2, 100), (3, 10), (1, 256)) if len(sys.argv) < 2 else [tuple(m
     ref = None
     lags = [int(v) for v in os.environ.get("SWEEP_LAG", "1").split(",")]
     Gs = ((0, 1, 2, 3, 4) if cfg != 1 else (0, 4, 8, 12, 16, 24)) if os.environ.get("SWEEP_G") else (0,)
+    if os.environ.get("SWEEP_GS"):
+        Gs = tuple(int(v) for v in os.environ["SWEEP_GS"].split(","))
     for lag, G in [(l, g) for l in lags for g in Gs]:
         if G > nf:
             continue
