@@ -639,16 +639,25 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       const double Nsz = (double)a.fa.n_sz;
       const double lN = log2(Nsz);
       constexpr int PER = kNSlots / kFinTasks;
+      constexpr int NIT = (PER + NC - 1) / NC;
       double acc = 0.0;
       unsigned long long novf = 0;
-      for (int s = id * PER + tid; s < (id + 1) * PER; s += NC) {
-        const unsigned int c = __ldcg(gh + s);
+      // every load first (one L2 round trip instead of one per bin), then the bins in the
+      // same order as before (the per-thread sum order, hence the result, is unchanged)
+      unsigned int cv[NIT];
+#pragma unroll
+      for (int k = 0; k < NIT; ++k)
+        cv[k] = (tid + k * NC < PER) ? __ldcg(gh + id * PER + tid + k * NC) : 0u;
+#pragma unroll
+      for (int k = 0; k < NIT; ++k) {
+        const int s = id * PER + tid + k * NC;
+        const unsigned int c = cv[k];
         if (c) {
           const double cd = (double)c;
           acc += cd * (lN - log2(cd));
           gh[s] = 0u;
         }
-        if (s == kOvfSlot) novf = c;
+        if (s == kOvfSlot && tid + k * NC < PER) novf = c;
       }
       const int np = a.nT * CW;
       const int per = (np + kFinTasks - 1) / kFinTasks;
