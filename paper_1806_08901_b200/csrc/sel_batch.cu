@@ -18,6 +18,9 @@
 // fields, and field f arrives in L2 two phases before its tiles.  Histogram/partial
 // buffers rotate over f % 3 (T(f) waits fin_ready[f-3]).  All floating-point sums
 // are per task and reduced in task order: results are bit-identical to the per-field path.
+// The sequence is decoded once on the host (build_group_sequence, cached per key) into a
+// 16-byte-per-task table the producer reads: decoding on the producer thread itself was
+// the kernel's critical path.
 #include <vector>
 
 #include "sel_tile_common.cuh"
