@@ -84,6 +84,9 @@ typedef struct {
   int32_t status;            /* sel_status of this field (batch calls)                        */
   int32_t choice_eb;         /* selection based on the error bound (Lu et al.): the  */
                              /* lower bit-rate at the user's eb, 0 = SZ iff BR_sz < BR_zfp    */
+  uint64_t hist_total;       /* sum of the 65,536 histogram counts as the finalize read them  */
+                             /* on the device (== n_sz_points unless a count was lost)        */
+  uint64_t hist_ovf;         /* count in the overflow slot 65,535, device-counted              */
 } sel_result;
 
 /* Create a plan for fields of shape dims[0..ndims-1].
@@ -108,6 +111,9 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double e
  *   "groups"          k_batch CTA groups, 0 (default) = automatic, else 1..148
  *   "lag"             k_batch phases between a field's range pass and its tiles, 1..4
  *                     (default 2)
+ *   "batch_debug"     1 = the persistent k_batch kernel also dumps, per field, the
+ *                     histogram its finalize tasks read and its per-(task, part) partials
+ *                     (sel_debug_copy "batch_hist" / "batch_part"; tests)
  * None changes any result (tests).  Errors: SEL_EINVAL (unknown key, value out of range). */
 int sel_set_option(sel_plan_t plan, const char *key, double value);
 
@@ -161,8 +167,21 @@ int sel_choose_eb(const sel_result *r, int32_t *choice);
  *   "uword"  uint32[n_blocks*4^d] negabinary words, sequency order
  *   "bits"   uint32[n_blocks]
  *   "err"    double[n_blocks]   E_b
+ * and of the LAST k_batch launch (requires option batch_debug=1; nf = its field count):
+ *   "batch_hist" uint32[nf][65536] each field's histogram as the finalize tasks read it
+ *   "batch_part" {uint64 bits, double err}[nf][nT * parts_per_task] per-(tile task, part)
+ *                sums of the ZFP block bits / errors, layout from sel_batch_layout
  * bytes must equal the array size.  Errors: SEL_EINVAL, SEL_ECUDA. */
 int sel_debug_copy(sel_plan_t plan, const char *what, void *host_dst, uint64_t bytes);
+
+/* Test-only: geometry of the k_batch partials of this plan, out[0..7] =
+ *   {nT tile tasks per field, parts per task, block rows per part, block rows per tile,
+ *    tile columns ntk (32 blocks each), tile rows ntj, sampled (1: part p of task t covers
+ *    processed blocks 32*(t*parts+p) .. +31 in row-major order), CTA groups of the last
+ *    launch}.  Tile task t covers tile column t % ntk, tile row (t / ntk) % ntj, block
+ *    layer t / (ntk*ntj) (3D); part p of it the block rows [p*rows_per_part, +rows_per_part)
+ *    of the tile.  Errors: SEL_EINVAL (NULL). */
+int sel_batch_layout(sel_plan_t plan, int64_t out[8]);
 
 /* Per-kernel device time accumulated since the last reset (option kernel_timing=1):
  * ms[0] value range, ms[1] fused estimate, ms[2] finalize; launches[k] the count.

@@ -30,7 +30,7 @@ _LIB = os.path.join(_HERE, "liborc.so")
 _lock = threading.Lock()
 _lib = None
 
-CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+CFLAGS = ["-O2", "-std=gnu11", "-pthread", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-Wall", "-Wextra"]
 
 NSLOTS = 65536
@@ -50,7 +50,7 @@ def build(force: bool = False) -> str:
              os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC), os.path.getmtime(_HDR)))
     if force or stale:
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm", "-lpthread"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -66,10 +66,11 @@ class Result(C.Structure):
         ("n_sz_points", C.c_uint64), ("n_values", C.c_uint64), ("n_blocks", C.c_uint64),
         ("zfp_total_bits", C.c_uint64), ("zfp_err_sum", C.c_double),
         ("minexp", C.c_int32), ("r_f", C.c_float), ("choice_eb", C.c_int32),
+        ("pad_", C.c_int32), ("hist_total", C.c_uint64), ("hist_ovf", C.c_uint64),
     ]
 
     def to_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
 
 
 class Debug(C.Structure):
@@ -87,6 +88,9 @@ def lib():
             P = C.c_void_p
             L.orc_estimate.argtypes = [P, C.c_int, P, C.c_int, C.c_double, P, C.c_double, P, P]
             L.orc_estimate.restype = C.c_int
+            L.orc_estimate_mt.argtypes = [P, C.c_int, P, C.c_int, C.c_double, P, C.c_double, P, P,
+                                          C.c_int]
+            L.orc_estimate_mt.restype = C.c_int
             L.orc_processed_blocks.argtypes = [C.c_int, P, P]
             L.orc_processed_blocks.restype = C.c_uint64
             L.orc_lorenzo.argtypes = [P, C.c_int, P, P]
@@ -149,9 +153,20 @@ def processed_blocks(shape, stride=None) -> int:
     return int(lib().orc_processed_blocks(nd, _ptr(dims), None if st is None else _ptr(st)))
 
 
+def default_threads() -> int:
+    """Host cores this process may run on (the affinity set)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:  # pragma: no cover
+        return max(1, os.cpu_count() or 1)
+
+
 def estimate(x: np.ndarray, eb: float, mode: str = "rel", stride=None, sz_offset: float = 0.5,
-             debug: bool = False) -> dict:
-    """Alg. 1 lines 1-10 on a C-order float32 field."""
+             debug: bool = False, threads: int = 1) -> dict:
+    """Alg. 1 lines 1-10 on a C-order float32 field.
+
+    threads > 1 runs orc_estimate_mt: contiguous slabs of blocks per thread, exact merges,
+    bit-identical to threads = 1 (0 = every core of the affinity set)."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     nd, dims, st = _dims_stride(x.shape, stride)
     size = 4 ** nd
@@ -159,17 +174,22 @@ def estimate(x: np.ndarray, eb: float, mode: str = "rel", stride=None, sz_offset
     dbgs = None
     arrays = {}
     if debug:
+        # debug=True: every dump; or an iterable of names ("codes", "hist", "emax",
+        # "coef", "uword", "bits", "err") to keep memory bounded on full-size fields
+        want = {k for k, _ in Debug._fields_} if debug is True else set(debug)
         npb = processed_blocks(x.shape, stride)
-        arrays = {
-            "codes": np.empty(x.shape, np.int32), "hist": np.zeros(NSLOTS, np.uint64),
-            "emax": np.empty(npb, np.int32), "coef": np.empty((npb, size), np.int32),
-            "uword": np.empty((npb, size), np.uint32), "bits": np.empty(npb, np.uint32),
-            "err": np.empty(npb, np.float64),
+        spec = {
+            "codes": (x.shape, np.int32), "hist": ((NSLOTS,), np.uint64),
+            "emax": ((npb,), np.int32), "coef": ((npb, size), np.int32),
+            "uword": ((npb, size), np.uint32), "bits": ((npb,), np.uint32),
+            "err": ((npb,), np.float64),
         }
-        dbgs = Debug(*[_ptr(arrays[k]) for k, _ in Debug._fields_])
-    st_ = lib().orc_estimate(_ptr(x), nd, _ptr(dims), 1 if mode == "rel" else 0, float(eb),
-                             None if st is None else _ptr(st), float(sz_offset), C.byref(res),
-                             C.byref(dbgs) if dbgs is not None else None)
+        arrays = {k: (np.zeros if k == "hist" else np.empty)(spec[k][0], spec[k][1]) for k in want}
+        dbgs = Debug(*[_ptr(arrays[k]) if k in arrays else None for k, _ in Debug._fields_])
+    nthr = default_threads() if threads == 0 else int(threads)
+    st_ = lib().orc_estimate_mt(_ptr(x), nd, _ptr(dims), 1 if mode == "rel" else 0, float(eb),
+                                None if st is None else _ptr(st), float(sz_offset), C.byref(res),
+                                C.byref(dbgs) if dbgs is not None else None, nthr)
     if st_ != 0:
         raise OracleError(st_)
     out = res.to_dict()

@@ -9,6 +9,7 @@
 #include "orc.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -371,51 +372,64 @@ uint64_t orc_processed_blocks(int nd, const int64_t *dims, const int32_t *stride
 
 /* ------------------------------------------------------------------ */
 /* whole field: Alg. 1 lines 1-10                                       */
+/*                                                                      */
+/* The loop bodies below are the plain per-point / per-block steps.     */
+/* orc_estimate_mt splits the block grid into contiguous slabs of the   */
+/* slowest block axis, one per thread (the paper's one-process-per-     */
+/* field model, applied within a field); every merge is exact:   */
+/* integer histogram / count sums, and the per-block E_b are stored by  */
+/* processed-block ordinal and summed in that order after the join, so  */
+/* the result is bit-identical to nthreads = 1.                         */
 /* ------------------------------------------------------------------ */
-int orc_estimate(const float *x, int nd, const int64_t *dims, int eb_mode, double eb,
-                 const int32_t *stride, double sz_offset, orc_result *out, orc_debug *dbg) {
-  if (nd < 1 || nd > 3 || !x || !dims || !out) return ORC_EINVAL;
-  int64_t N = 1;
-  for (int a = 0; a < nd; ++a) { if (dims[a] < 1) return ORC_EINVAL; N *= dims[a]; }
-  int32_t s[3] = {1, 1, 1};
-  for (int a = 0; a < nd; ++a) { s[a] = stride ? stride[a] : 1; if (s[a] < 1) return ORC_EINVAL; }
-  if (!isfinite(eb) || !(eb > 0.0)) return ORC_EINVAL;
-  if (eb_mode != 0 && eb_mode != 1) return ORC_EINVAL;
+typedef struct {
+  /* inputs */
+  const float *x;
+  int nd;
+  const int64_t *dims;
+  int64_t nb[3];
+  int32_t s[3];
+  int size;
+  const int32_t *perm;
+  float r_f;
+  int32_t minexp;
+  orc_debug *dbg;
+  double *E;          /* [processed blocks] E_b by processed-block ordinal */
+  uint32_t *bitsv;    /* [processed blocks] bits_b */
+  /* slab of the slowest block axis */
+  int64_t b0_lo, b0_hi;
+  /* value-range part: element range */
+  int64_t i_lo, i_hi;
+  float vmin, vmax;
+  int bad;
+  /* outputs */
+  uint64_t *hist;
+  uint64_t n_sz, n_values, n_blocks;
+} orc_work;
 
-  /* A1: value range over the whole field (P:479) */
-  float vmin = x[0], vmax = x[0];
-  for (int64_t i = 0; i < N; ++i) {
-    if (!isfinite(x[i])) return ORC_ENONFINITE;
-    if (x[i] < vmin) vmin = x[i];
-    if (x[i] > vmax) vmax = x[i];
+/* A1 over x[i_lo, i_hi): min, max, non-finite flag */
+static void work_range(orc_work *w) {
+  w->bad = 0;
+  w->vmin = w->x[w->i_lo];
+  w->vmax = w->x[w->i_lo];
+  for (int64_t i = w->i_lo; i < w->i_hi; ++i) {
+    float v = w->x[i];
+    if (!isfinite(v)) { w->bad = 1; continue; }
+    if (v < w->vmin) w->vmin = v;
+    if (v > w->vmax) w->vmax = v;
   }
-  double VR = (double)vmax - (double)vmin;
+}
 
-  /* A2: error bound (Alg. 1 line 2, P:479) and derived scalars */
-  double eb_abs = (eb_mode == 1) ? eb * VR : eb;
-  if (eb_mode == 1 && VR == 0.0) return ORC_EDEGENERATE;
-  float r_f = (float)(1.0 / (2.0 * eb_abs));
-  if (!isfinite(r_f) || !(eb_abs > 0.0)) return ORC_EINVAL;
-  int fe; frexp(eb_abs, &fe);
-  int32_t minexp = fe - 1; /* floor(log2 eb_abs) */
-
-  int64_t nb[3] = {1, 1, 1};
-  for (int a = 0; a < nd; ++a) nb[a] = (dims[a] + 3) / 4;
-  int size = (int)ipow4(nd);
-  int32_t perm[64];
-  orc_sequency_perm(nd, perm);
-
-  uint64_t *hist = (uint64_t *)calloc(ORC_NSLOTS, sizeof(uint64_t));
-  if (!hist) return ORC_EINVAL;
-  if (dbg && dbg->codes) for (int64_t i = 0; i < N; ++i) dbg->codes[i] = -1;
-
-  uint64_t n_sz = 0, n_values = 0, n_blocks = 0, total_bits = 0;
-  double err_sum = 0.0;
-  int64_t pb = 0; /* processed-block ordinal */
-
+/* A3-A14 for the processed blocks with b0 in [b0_lo, b0_hi), row-major */
+static void work_blocks(orc_work *w) {
+  const int nd = w->nd, size = w->size;
+  const int64_t *dims = w->dims;
+  const int64_t *nb = w->nb;
+  const int32_t *s = w->s;
+  /* processed-block ordinal of the first block of the slab */
+  int64_t npb12 = ((nb[1] + s[1] - 1) / s[1]) * ((nb[2] + s[2] - 1) / s[2]);
+  int64_t pb = ((w->b0_lo + s[0] - 1) / s[0]) * npb12;
   int64_t b[3];
-  int64_t nblk_total = nb[0] * nb[1] * nb[2];
-  for (int64_t lb = 0; lb < nblk_total; ++lb) {
+  for (int64_t lb = w->b0_lo * nb[1] * nb[2]; lb < w->b0_hi * nb[1] * nb[2]; ++lb) {
     /* block coordinates, row-major (axis 0 slowest) */
     int64_t r = lb;
     for (int a = nd - 1; a >= 0; --a) { b[a] = r % nb[a]; r /= nb[a]; }
@@ -437,20 +451,20 @@ int orc_estimate(const float *x, int nd, const int64_t *dims, int eb_mode, doubl
       }
       int64_t lin = 0;
       for (int a = 0; a < nd; ++a) lin = lin * dims[a] + cl[a];
-      blk[n] = x[lin];
+      blk[n] = w->x[lin];
       if (!inside) continue;
       ++nreal;
       int origin = 1;
       for (int a = 0; a < nd; ++a) if (idx[a] != 0) origin = 0;
       if (origin) continue; /* R4: the first value is stored verbatim */
-      float d = orc_lorenzo(x, nd, dims, idx);
-      int32_t slot = orc_quantize(d, r_f);
-      hist[slot] += 1;
-      ++n_sz;
-      if (dbg && dbg->codes) dbg->codes[lin] = slot;
+      float d = orc_lorenzo(w->x, nd, dims, idx);
+      int32_t slot = orc_quantize(d, w->r_f);
+      w->hist[slot] += 1;
+      ++w->n_sz;
+      if (w->dbg && w->dbg->codes) w->dbg->codes[lin] = slot;
     }
-    n_values += (uint64_t)nreal;
-    ++n_blocks;
+    w->n_values += (uint64_t)nreal;
+    ++w->n_blocks;
 
     /* ---- ZFP part: A9-A14 on the (padded) block ---- */
     int32_t emax = orc_block_emax(blk, size);
@@ -464,58 +478,163 @@ int orc_estimate(const float *x, int nd, const int64_t *dims, int eb_mode, doubl
     } else {
       orc_block_bfp(blk, size, emax, coef);
       orc_fwd_xform(coef, nd);
-      for (int j = 0; j < size; ++j) u[j] = orc_negabinary(coef[perm[j]]);
-      int32_t p = orc_precision(emax, minexp, nd);
+      for (int j = 0; j < size; ++j) u[j] = orc_negabinary(coef[w->perm[j]]);
+      int32_t p = orc_precision(emax, w->minexp, nd);
       int kmin = 32 - p;
       bits = (p == 0) ? 1 : 9 + orc_gt_count(u, size, kmin);
-      E = orc_block_err(coef, u, perm, nd, kmin, emax);
+      E = orc_block_err(coef, u, w->perm, nd, kmin, emax);
     }
-    total_bits += bits;
-    err_sum += E;
-    if (dbg) {
-      if (dbg->emax) dbg->emax[pb] = emax;
-      if (dbg->coef) memcpy(dbg->coef + pb * size, coef, sizeof(int32_t) * size);
-      if (dbg->uword) memcpy(dbg->uword + pb * size, u, sizeof(uint32_t) * size);
-      if (dbg->bits) dbg->bits[pb] = (uint32_t)bits;
-      if (dbg->err) dbg->err[pb] = E;
+    w->E[pb] = E;
+    w->bitsv[pb] = (uint32_t)bits;
+    if (w->dbg) {
+      if (w->dbg->emax) w->dbg->emax[pb] = emax;
+      if (w->dbg->coef) memcpy(w->dbg->coef + pb * size, coef, sizeof(int32_t) * size);
+      if (w->dbg->uword) memcpy(w->dbg->uword + pb * size, u, sizeof(uint32_t) * size);
+      if (w->dbg->bits) w->dbg->bits[pb] = (uint32_t)bits;
+      if (w->dbg->err) w->dbg->err[pb] = E;
     }
     ++pb;
   }
+}
 
-  if (n_sz == 0) { free(hist); return ORC_EDEGENERATE; }
+static void *work_range_thread(void *p) { work_range((orc_work *)p); return NULL; }
+static void *work_blocks_thread(void *p) { work_blocks((orc_work *)p); return NULL; }
 
-  /* A6: entropy bit-rate (Eq. entropy, bitrate-sz P:402), +0.5 offset */
-  double H = orc_entropy_counts(hist, ORC_NSLOTS);
-  double p_ovf = (double)hist[ORC_OVF_SLOT] / (double)n_sz;
-  double br_sz = H + sz_offset + 32.0 * p_ovf;
-  /* A7: Eq. (psnr-sz) */
-  double psnr_sz = 20.0 * log10(VR / eb_abs) + 10.0 * log10(3.0);
-  /* A13/A15: EC bit-rate; A14 PSNR_sp */
-  double br_zfp = (double)total_bits / (double)n_values;
-  double mse = err_sum / (double)n_values;
-  double psnr_zfp = (mse > 0.0) ? 20.0 * log10(VR) - 10.0 * log10(mse) : INFINITY;
+/* run fn over w[0..n) on n threads (w[0] on the caller's thread) */
+static void run_threads(orc_work *w, int n, void *(*fn)(void *)) {
+  pthread_t th[ORC_MAX_THREADS];
+  int started[ORC_MAX_THREADS];
+  for (int t = 1; t < n; ++t) started[t] = pthread_create(&th[t], NULL, fn, &w[t]) == 0;
+  fn(&w[0]);
+  for (int t = 1; t < n; ++t) {
+    if (started[t]) pthread_join(th[t], NULL);
+    else fn(&w[t]);   /* could not start a thread: run it here (same result) */
+  }
+}
 
-  memset(out, 0, sizeof(*out));
-  out->sz_bits_per_value = br_sz;
-  out->sz_psnr = psnr_sz;
-  out->zfp_bits_per_value = br_zfp;
-  out->zfp_psnr = psnr_zfp;
-  out->value_range = VR;
-  out->eb_abs = eb_abs;
-  out->sz_entropy = H;
-  out->sz_overflow_frac = p_ovf;
-  out->zfp_mse = mse;
-  out->n_sz_points = n_sz;
-  out->n_values = n_values;
-  out->n_blocks = n_blocks;
-  out->zfp_total_bits = total_bits;
-  out->zfp_err_sum = err_sum;
-  out->minexp = minexp;
-  out->r_f = r_f;
-  out->choice = orc_select(br_sz, psnr_sz, br_zfp, psnr_zfp, VR, eb_abs, mse,
-                           &out->sz_bits_matched, &out->sz_eb_matched, &out->matched);
-  out->choice_eb = orc_select_eb(br_sz, br_zfp);
-  if (dbg && dbg->hist) memcpy(dbg->hist, hist, sizeof(uint64_t) * ORC_NSLOTS);
+int orc_estimate_mt(const float *x, int nd, const int64_t *dims, int eb_mode, double eb,
+                    const int32_t *stride, double sz_offset, orc_result *out, orc_debug *dbg,
+                    int nthreads) {
+  if (nd < 1 || nd > 3 || !x || !dims || !out) return ORC_EINVAL;
+  int64_t N = 1;
+  for (int a = 0; a < nd; ++a) { if (dims[a] < 1) return ORC_EINVAL; N *= dims[a]; }
+  int32_t s[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) { s[a] = stride ? stride[a] : 1; if (s[a] < 1) return ORC_EINVAL; }
+  if (!isfinite(eb) || !(eb > 0.0)) return ORC_EINVAL;
+  if (eb_mode != 0 && eb_mode != 1) return ORC_EINVAL;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > ORC_MAX_THREADS) nthreads = ORC_MAX_THREADS;
+
+  int64_t nb[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) nb[a] = (dims[a] + 3) / 4;
+  int nt = nthreads;
+  if (nt > nb[0]) nt = (int)nb[0];
+  if ((int64_t)nt > N) nt = (int)N;
+  orc_work w[ORC_MAX_THREADS];
+  memset(w, 0, sizeof(w));
+
+  /* A1: value range over the whole field (P:479) */
+  for (int t = 0; t < nt; ++t) {
+    w[t].x = x;
+    w[t].i_lo = N * t / nt;
+    w[t].i_hi = N * (t + 1) / nt;
+  }
+  run_threads(w, nt, work_range_thread);
+  float vmin = w[0].vmin, vmax = w[0].vmax;
+  for (int t = 0; t < nt; ++t) {
+    if (w[t].bad) return ORC_ENONFINITE;
+    if (w[t].vmin < vmin) vmin = w[t].vmin;
+    if (w[t].vmax > vmax) vmax = w[t].vmax;
+  }
+  double VR = (double)vmax - (double)vmin;
+
+  /* A2: error bound (Alg. 1 line 2, P:479) and derived scalars */
+  double eb_abs = (eb_mode == 1) ? eb * VR : eb;
+  if (eb_mode == 1 && VR == 0.0) return ORC_EDEGENERATE;
+  float r_f = (float)(1.0 / (2.0 * eb_abs));
+  if (!isfinite(r_f) || !(eb_abs > 0.0)) return ORC_EINVAL;
+  int fe; frexp(eb_abs, &fe);
+  int32_t minexp = fe - 1; /* floor(log2 eb_abs) */
+
+  int size = (int)ipow4(nd);
+  int32_t perm[64];
+  orc_sequency_perm(nd, perm);
+  uint64_t npb = orc_processed_blocks(nd, dims, stride);
+
+  int rc = ORC_OK;
+  uint64_t *hist = (uint64_t *)calloc((size_t)ORC_NSLOTS * nt, sizeof(uint64_t));
+  double *E = (double *)malloc(sizeof(double) * (npb ? npb : 1));
+  uint32_t *bitsv = (uint32_t *)malloc(sizeof(uint32_t) * (npb ? npb : 1));
+  if (!hist || !E || !bitsv) { rc = ORC_EINVAL; goto done; }
+  if (dbg && dbg->codes) for (int64_t i = 0; i < N; ++i) dbg->codes[i] = -1;
+
+  for (int t = 0; t < nt; ++t) {
+    w[t].nd = nd; w[t].dims = dims; w[t].size = size; w[t].perm = perm;
+    for (int a = 0; a < 3; ++a) { w[t].nb[a] = nb[a]; w[t].s[a] = s[a]; }
+    w[t].r_f = r_f; w[t].minexp = minexp; w[t].dbg = dbg; w[t].E = E; w[t].bitsv = bitsv;
+    w[t].b0_lo = nb[0] * t / nt;
+    w[t].b0_hi = nb[0] * (t + 1) / nt;
+    w[t].hist = hist + (size_t)ORC_NSLOTS * t;
+  }
+  run_threads(w, nt, work_blocks_thread);
+
+  /* exact merges: integer sums; E_b and bits_b in processed-block order */
+  uint64_t n_sz = 0, n_values = 0, n_blocks = 0, total_bits = 0;
+  for (int t = 0; t < nt; ++t) {
+    n_sz += w[t].n_sz; n_values += w[t].n_values; n_blocks += w[t].n_blocks;
+    if (t > 0)
+      for (int k = 0; k < ORC_NSLOTS; ++k) hist[k] += w[t].hist[k];
+  }
+  double err_sum = 0.0;
+  for (uint64_t pb = 0; pb < npb; ++pb) { total_bits += bitsv[pb]; err_sum += E[pb]; }
+
+  if (n_sz == 0) { rc = ORC_EDEGENERATE; goto done; }
+  {
+    /* A6: entropy bit-rate (Eq. entropy, bitrate-sz P:402), +0.5 offset */
+    double H = orc_entropy_counts(hist, ORC_NSLOTS);
+    double p_ovf = (double)hist[ORC_OVF_SLOT] / (double)n_sz;
+    double br_sz = H + sz_offset + 32.0 * p_ovf;
+    /* A7: Eq. (psnr-sz) */
+    double psnr_sz = 20.0 * log10(VR / eb_abs) + 10.0 * log10(3.0);
+    /* A13/A15: EC bit-rate; A14 PSNR_sp */
+    double br_zfp = (double)total_bits / (double)n_values;
+    double mse = err_sum / (double)n_values;
+    double psnr_zfp = (mse > 0.0) ? 20.0 * log10(VR) - 10.0 * log10(mse) : INFINITY;
+
+    memset(out, 0, sizeof(*out));
+    out->sz_bits_per_value = br_sz;
+    out->sz_psnr = psnr_sz;
+    out->zfp_bits_per_value = br_zfp;
+    out->zfp_psnr = psnr_zfp;
+    out->value_range = VR;
+    out->eb_abs = eb_abs;
+    out->sz_entropy = H;
+    out->sz_overflow_frac = p_ovf;
+    out->zfp_mse = mse;
+    out->n_sz_points = n_sz;
+    out->n_values = n_values;
+    out->n_blocks = n_blocks;
+    out->zfp_total_bits = total_bits;
+    out->zfp_err_sum = err_sum;
+    out->minexp = minexp;
+    out->r_f = r_f;
+    out->choice = orc_select(br_sz, psnr_sz, br_zfp, psnr_zfp, VR, eb_abs, mse,
+                             &out->sz_bits_matched, &out->sz_eb_matched, &out->matched);
+    out->choice_eb = orc_select_eb(br_sz, br_zfp);
+    uint64_t tot = 0;
+    for (int k = 0; k < ORC_NSLOTS; ++k) tot += hist[k];
+    out->hist_total = tot;
+    out->hist_ovf = hist[ORC_OVF_SLOT];
+    if (dbg && dbg->hist) memcpy(dbg->hist, hist, sizeof(uint64_t) * ORC_NSLOTS);
+  }
+done:
   free(hist);
-  return ORC_OK;
+  free(E);
+  free(bitsv);
+  return rc;
+}
+
+int orc_estimate(const float *x, int nd, const int64_t *dims, int eb_mode, double eb,
+                 const int32_t *stride, double sz_offset, orc_result *out, orc_debug *dbg) {
+  return orc_estimate_mt(x, nd, dims, eb_mode, eb, stride, sz_offset, out, dbg, 1);
 }

@@ -37,6 +37,9 @@ typedef struct {
   int32_t minexp;
   float r_f;
   int32_t choice_eb;    /* selection based on the error bound (Lu et al.) */
+  int32_t pad_;
+  uint64_t hist_total;  /* sum of the 65,536 histogram counts (== n_sz_points) */
+  uint64_t hist_ovf;    /* count in the overflow slot 65,535 */
 } orc_result;
 
 /* Optional per-element dumps (any pointer may be NULL).
@@ -61,6 +64,13 @@ typedef struct {
 int orc_estimate(const float *x, int ndims, const int64_t *dims, int eb_mode,
                  double eb, const int32_t *stride, double sz_offset,
                  orc_result *out, orc_debug *dbg);
+/* Same, on nthreads threads (contiguous slabs of the slowest block axis); every
+ * merge is exact and the per-block E_b are summed in block order, so the result is
+ * bit-identical to orc_estimate (checked by tests/test_oracle_pins.py). */
+#define ORC_MAX_THREADS 256
+int orc_estimate_mt(const float *x, int ndims, const int64_t *dims, int eb_mode,
+                    double eb, const int32_t *stride, double sz_offset,
+                    orc_result *out, orc_debug *dbg, int nthreads);
 uint64_t orc_processed_blocks(int ndims, const int64_t *dims, const int32_t *stride);
 
 /* ---- single steps, exported for the pin tests ---- */

@@ -24,7 +24,8 @@ EB_ABS, EB_REL = 0, 1
 
 # every entry point declared in include/sel.h
 EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_batch",
-           "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_choose_eb", "sel_debug_copy", "sel_kernel_times",
+           "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_choose_eb",
+           "sel_debug_copy", "sel_batch_layout", "sel_kernel_times",
            "sel_processed_blocks", "sel_processed_values", "sel_workspace_bytes",
            "sel_launch_count", "sel_plan_destroy", "sel_strerror")
 
@@ -47,7 +48,7 @@ class Result(C.Structure):
         ("n_sz_points", C.c_uint64), ("n_values", C.c_uint64), ("n_blocks", C.c_uint64),
         ("zfp_total_bits", C.c_uint64), ("zfp_err_sum", C.c_double),
         ("minexp", C.c_int32), ("r_f", C.c_float), ("status", C.c_int32),
-        ("choice_eb", C.c_int32),
+        ("choice_eb", C.c_int32), ("hist_total", C.c_uint64), ("hist_ovf", C.c_uint64),
     ]
 
     def to_dict(self) -> dict:
@@ -84,6 +85,8 @@ def lib():
         L.sel_choose_eb.restype = C.c_int
         L.sel_debug_copy.argtypes = [P, C.c_char_p, P, C.c_uint64]
         L.sel_debug_copy.restype = C.c_int
+        L.sel_batch_layout.argtypes = [P, P]
+        L.sel_batch_layout.restype = C.c_int
         L.sel_kernel_times.argtypes = [P, P, P, C.c_int]
         L.sel_kernel_times.restype = C.c_int
         for f in ("sel_processed_blocks", "sel_processed_values", "sel_launch_count"):
@@ -115,27 +118,50 @@ def _stream_ptr(stream):
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _device_ptr(t) -> int:
+def _numel(shape) -> int:
+    n = 1
+    for s in shape:
+        n *= int(s)
+    return n
+
+
+def _device_ptr(t, shape=None, device=None) -> int:
+    """Pointer of a contiguous float32 CUDA tensor holding prod(shape) values on the
+    current device (the C ABI reads exactly prod(plan dims) floats from it)."""
     import torch
     if not isinstance(t, torch.Tensor):
         raise TypeError("expected a torch.Tensor on a CUDA device")
     if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
         raise ValueError("field must be a contiguous float32 CUDA tensor")
+    if shape is not None and t.numel() != _numel(shape):
+        raise ValueError(f"field has {t.numel()} values, the plan's shape {tuple(shape)} needs "
+                         f"{_numel(shape)}")
+    dev = torch.cuda.current_device() if device is None else device
+    if t.device.index != dev:
+        raise ValueError(f"field is on {t.device}, the plan runs on cuda:{dev}")
     return t.data_ptr()
 
 
-def _host_ptr(a) -> int:
+def _host_ptr(a, shape=None) -> int:
+    n = None
     try:
         import torch
         if isinstance(a, torch.Tensor):
             if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous():
                 raise ValueError("host field must be a contiguous float32 CPU tensor")
-            return a.data_ptr()
+            n = a.numel()
+            ptr = a.data_ptr()
     except ImportError:  # pragma: no cover
         pass
-    if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous):
-        raise ValueError("host field must be a C-contiguous float32 array")
-    return a.ctypes.data
+    if n is None:
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous):
+            raise ValueError("host field must be a C-contiguous float32 array")
+        n = a.size
+        ptr = a.ctypes.data
+    if shape is not None and n != _numel(shape):
+        raise ValueError(f"host field has {n} values, the plan's shape {tuple(shape)} needs "
+                         f"{_numel(shape)}")
+    return ptr
 
 
 class Plan:
@@ -150,6 +176,13 @@ class Plan:
         self._dims = (C.c_int64 * max(self.ndims, 1))(*shape)
         self._stride = None if stride is None else (C.c_int32 * self.ndims)(*[int(s) for s in stride])
         self._h = C.c_void_p()
+        self.device = None            # the CUDA device the plan's workspace lives on
+        try:
+            import torch
+            if torch.cuda.is_available():
+                self.device = torch.cuda.current_device()
+        except ImportError:  # pragma: no cover
+            pass
         m = EB_REL if mode == "rel" else EB_ABS
         if mode not in ("rel", "abs"):
             raise ValueError("mode must be 'rel' or 'abs'")
@@ -186,13 +219,13 @@ class Plan:
     # -- estimates
     def estimate(self, field, stream=None) -> dict:
         r = Result()
-        _check(lib().sel_estimate(self._h, C.c_void_p(_device_ptr(field)), _stream_ptr(stream),
+        _check(lib().sel_estimate(self._h, C.c_void_p(_device_ptr(field, self.shape, self.device)), _stream_ptr(stream),
                                   C.byref(r)))
         return r.to_dict()
 
     def estimate_batch(self, fields, stream=None) -> list[dict]:
         n = len(fields)
-        ptrs = (C.c_void_p * n)(*[_device_ptr(f) for f in fields])
+        ptrs = (C.c_void_p * n)(*[_device_ptr(f, self.shape, self.device) for f in fields])
         out = (Result * n)()
         _check(lib().sel_estimate_batch(self._h, ptrs, n, _stream_ptr(stream), out))
         return [o.to_dict() for o in out]
@@ -204,7 +237,7 @@ class Plan:
         n = len(fields)
         if out.numel() < n * C.sizeof(Result):
             raise ValueError("results buffer too small")
-        ptrs = (C.c_void_p * n)(*[_device_ptr(f) for f in fields])
+        ptrs = (C.c_void_p * n)(*[_device_ptr(f, self.shape, self.device) for f in fields])
         _check(lib().sel_estimate_batch_async(self._h, ptrs, n, _stream_ptr(stream),
                                               C.c_void_p(out.data_ptr())))
 
@@ -226,7 +259,7 @@ class Plan:
 
     def estimate_batch_host(self, fields, stream=None) -> list[dict]:
         n = len(fields)
-        ptrs = (C.c_void_p * n)(*[_host_ptr(f) for f in fields])
+        ptrs = (C.c_void_p * n)(*[_host_ptr(f, self.shape) for f in fields])
         out = (Result * n)()
         _check(lib().sel_estimate_batch_host(self._h, ptrs, n, _stream_ptr(stream), out))
         return [o.to_dict() for o in out]
@@ -240,6 +273,29 @@ class Plan:
                 "err": (np.float64, (B,))}[what]
         a = np.empty(spec[1], spec[0])
         _check(lib().sel_debug_copy(self._h, what.encode(), a.ctypes.data_as(C.c_void_p), a.nbytes))
+        return a
+
+    def batch_layout(self) -> dict:
+        o = (C.c_int64 * 8)()
+        _check(lib().sel_batch_layout(self._h, o))
+        keys = ("n_tasks", "parts_per_task", "rows_per_part", "rows_per_tile", "ntk", "ntj",
+                "sampled", "groups")
+        return dict(zip(keys, [int(v) for v in o]))
+
+    def batch_debug_copy(self, what: str, nf: int) -> np.ndarray:
+        """k_batch dumps of the last batch launch (option batch_debug=1): "hist" ->
+        uint32[nf, 65536]; "part" -> structured [nf, n_tasks * parts_per_task] of
+        (bits u64, err f64)."""
+        lay = self.batch_layout()
+        if what == "hist":
+            a = np.empty((nf, 65536), np.uint32)
+        elif what == "part":
+            a = np.empty((nf, lay["n_tasks"] * lay["parts_per_task"]),
+                         np.dtype([("bits", np.uint64), ("err", np.float64)]))
+        else:
+            raise ValueError(what)
+        _check(lib().sel_debug_copy(self._h, ("batch_" + what).encode(),
+                                    a.ctypes.data_as(C.c_void_p), a.nbytes))
         return a
 
     def close(self):

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "sel_internal.h"
@@ -57,6 +58,11 @@ struct sel_plan_st {
   int use_batch = 1;
   int groups = 0;                 // k_batch CTA groups (0: auto, batch_groups)
   int lag_t = 2;                  // k_batch phases from a field's range pass to its tiles
+  int batch_debug = 0;            // k_batch test dumps (histograms, partials) per field
+  BatchDump bdump;
+  int bdump_cap = 0;              // fields the dump buffers hold
+  int last_batch_nf = 0;          // fields of the last k_batch launch
+  int last_batch_G = 0;
   void *bstate = nullptr;                         // batch kernel state (grows with n)
   BatchTable btab;                                // k_batch task table (device, cached)
   cudaEvent_t bev[2] = {nullptr, nullptr};        // kernel_timing around k_batch
@@ -82,6 +88,7 @@ struct sel_plan_st {
 
   // end-to-end staging
   float *d_stage[2] = {nullptr, nullptr};
+  size_t stage_cap = 0;                           // bytes of each staging buffer
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
@@ -204,6 +211,9 @@ int enqueue_est(sel_plan_t p, const float *x, int f, cudaStream_t st, TimingSlot
 bool batch_ok(sel_plan_t p, const float *const *x, int n) {
   if (!(p->tile_ok || p->sampled_ok) || !p->use_batch || p->debug) return false;
   if (p->geo.N >= (int64_t)1 << 32) return false;   // k_batch histograms are u32
+  // task-table limits (16-bit tile coordinates, 32-bit task indices): otherwise the
+  // per-field kernels run the shape
+  if (!batch_fits(p->geo, p->tl[0], p->bs, n)) return false;
   for (int f = 0; f < n; ++f)
     if (((uintptr_t)x[f] & 15u) != 0) return false;
   return true;
@@ -222,13 +232,22 @@ int batch_groups(sel_plan_t p, int n) {
     if (p->sampled_ok && G < 16) G = 16;
     if (G > 64) G = 64;             // (C1, 256 small fields: 32 -> 64 groups +4 %)
     if (G > n / 2) G = n / 2;     // keep >= 2 fields per group (tail balance)
+    // CTAs join group blockIdx % G and fields are split evenly over the groups, so a G
+    // that does not divide the SM count leaves the smaller groups setting the makespan
+    // (G = 64 on 148 SMs: 2- and 3-CTA groups): snap larger G to a divisor
+    if (G > 8) {
+      int d = G;
+      while (d > 1 && p->sm_count % d != 0) --d;
+      if (2 * d >= G) G = d;
+    }
   }
   if (G > n) G = n;
   if (G > p->sm_count) G = p->sm_count;
   return G < 1 ? 1 : G;
 }
 
-int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
+int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st,
+                  sel_result *d_res = nullptr) {
   const int G = batch_groups(p, n);
   const size_t need = batch_state_bytes(n, p->bs, batch_ntasks(p->geo, p->tl[0], p->bs), G);
   if (need > p->bstate_cap) {
@@ -240,7 +259,27 @@ int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
     p->bstate_cap = 0;
     if (cudaMalloc(&p->bstate, need) != cudaSuccess) return SEL_ENOMEM;
     p->bstate_cap = need;
+    // zero once (the histogram ring stays zero between launches: the F tasks re-zero it)
+    CK(cudaMemsetAsync(p->bstate, 0, need, st));
   }
+  BatchDump dump;
+  if (p->batch_debug) {
+    if (n > p->bdump_cap) {
+      CK(cudaStreamSynchronize(st));
+      if (p->bdump.hist) cudaFree(p->bdump.hist);
+      if (p->bdump.part) cudaFree(p->bdump.part);
+      p->bdump = BatchDump();
+      p->bdump_cap = 0;
+      const size_t np = (size_t)batch_ntasks(p->geo, p->tl[0], p->bs) * batch_parts_per_task(p->geo);
+      if (cudaMalloc(&p->bdump.hist, (size_t)n * kNSlots * 4) != cudaSuccess ||
+          cudaMalloc(&p->bdump.part, (size_t)n * np * sizeof(Partial)) != cudaSuccess)
+        return SEL_ENOMEM;
+      p->bdump_cap = n;
+    }
+    dump = p->bdump;
+  }
+  p->last_batch_nf = n;
+  p->last_batch_G = G;
   FinalizeArgs fa;
   fa.mode = p->mode;
   fa.eb = p->eb;
@@ -258,8 +297,10 @@ int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st) {
     }
   }
   int rc = launch_batch(g, p->tl[0], p->bs, x, n, p->bstate, p->bstate_cap, fa, p->mode, p->eb,
-                        p->d_res, p->sm_count, G, p->lag_t, &p->btab, st, p->timing ? p->bev : nullptr);
-  if (rc) return cuda_fail(cudaGetLastError(), "k_batch launch");
+                        d_res ? d_res : p->d_res, p->sm_count, G, p->lag_t, &p->btab, dump, st,
+                        p->timing ? p->bev : nullptr);
+  if (rc == SEL_ECUDA) return cuda_fail(cudaGetLastError(), "k_batch launch");
+  if (rc) return rc;
   p->launches += 1;
   p->batch_timed = p->timing;
   return SEL_OK;
@@ -471,7 +512,7 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double e
     o_fp[k] = take((size_t)kFinCTAs * 8);
     o_fe[k] = take((size_t)kFinCTAs * 8);
     o_fb[k] = take((size_t)kFinCTAs * 8);
-    o_fo[k] = take(8);
+    o_fo[k] = take(16);   // [0] overflow count, [1] histogram total
     o_tk[k] = take(2 * 4);
   }
   if (cudaMalloc(&p->ws_mem, off) != cudaSuccess) {
@@ -525,6 +566,10 @@ int sel_set_option(sel_plan_t p, const char *key, double value) {
   if (!strcmp(key, "groups")) {
     if (!(value >= 0.0 && value <= 148.0)) return SEL_EINVAL;
     p->groups = (int)value;
+    return SEL_OK;
+  }
+  if (!strcmp(key, "batch_debug")) {
+    p->batch_debug = value != 0.0;
     return SEL_OK;
   }
   if (!strcmp(key, "batch_kernel")) {
@@ -617,16 +662,49 @@ int sel_estimate_batch_host(sel_plan_t p, const float *const *h_fields, int n, v
       CK(cudaEventCreateWithFlags(&p->ev_done[b], cudaEventDisableTiming));
     }
   }
-  for (int b = 0; b < 2; ++b)
-    if (!p->d_stage[b] && cudaMalloc(&p->d_stage[b], bytes) != cudaSuccess) return SEL_ENOMEM;
-  // double-buffered: copy of field f+1 (copy stream) overlaps the estimate of f
-  for (int f = 0; f < n; ++f) {
-    const int b = f & 1;
-    if (f >= 2) CK(cudaStreamWaitEvent(p->copy_stream, p->ev_done[b], 0));
-    CK(cudaMemcpyAsync(p->d_stage[b], h_fields[f], bytes, cudaMemcpyHostToDevice, p->copy_stream));
+  // Chunks of K fields (<= ~1 GB per staging buffer), double-buffered: the H2D copies of
+  // chunk c+1 (copy stream) overlap the estimate of chunk c, which is ONE k_batch launch
+  // over the chunk -- the same kernel as the device-resident entry points -- where the
+  // shape allows it (else the per-field kernels, one field at a time).
+  const bool kb = (p->tile_ok || p->sampled_ok) && p->use_batch && !p->debug && !p->timing &&
+                  p->geo.N < ((int64_t)1 << 32) && (p->geo.N % 4 == 0);
+  int K = 1;
+  if (kb) {
+    K = (int)std::max<size_t>(1, (size_t)1e9 / bytes);
+    if (K > n) K = n;
+  }
+  if (p->stage_cap < (size_t)K * bytes) {
+    if (p->d_stage[0] || p->d_stage[1]) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaStreamSynchronize(p->copy_stream));
+    }
+    for (int b = 0; b < 2; ++b) {
+      if (p->d_stage[b]) cudaFree(p->d_stage[b]);
+      p->d_stage[b] = nullptr;
+    }
+    p->stage_cap = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaMalloc(&p->d_stage[b], (size_t)K * bytes) != cudaSuccess) return SEL_ENOMEM;
+    p->stage_cap = (size_t)K * bytes;
+  }
+  std::vector<const float *> ptrs((size_t)K);
+  const int nchunk = (n + K - 1) / K;
+  for (int c = 0; c < nchunk; ++c) {
+    const int b = c & 1, f0 = c * K, nfc = std::min(K, n - f0);
+    if (c >= 2) CK(cudaStreamWaitEvent(p->copy_stream, p->ev_done[b], 0));
+    for (int i = 0; i < nfc; ++i) {
+      float *dst = p->d_stage[b] + (size_t)i * (size_t)p->geo.N;
+      CK(cudaMemcpyAsync(dst, h_fields[f0 + i], bytes, cudaMemcpyHostToDevice, p->copy_stream));
+      ptrs[(size_t)i] = dst;
+    }
     CK(cudaEventRecord(p->ev_copied[b], p->copy_stream));
     CK(cudaStreamWaitEvent(st, p->ev_copied[b], 0));
-    if ((rc = enqueue_field(p, p->d_stage[b], st, f))) return rc;
+    if (kb && batch_ok(p, ptrs.data(), nfc)) {
+      if ((rc = enqueue_batch(p, ptrs.data(), nfc, st, p->d_res + f0))) return rc;
+    } else {
+      for (int i = 0; i < nfc; ++i)
+        if ((rc = enqueue_field(p, ptrs[(size_t)i], st, f0 + i))) return rc;
+    }
     CK(cudaEventRecord(p->ev_done[b], st));
   }
   return finish(p, st, n, out);
@@ -654,7 +732,21 @@ int sel_choose_eb(const sel_result *r, int32_t *choice) {
 }
 
 int sel_debug_copy(sel_plan_t p, const char *what, void *dst, uint64_t bytes) {
-  if (!p || !what || !dst || !p->dbg_mem) return SEL_EINVAL;
+  if (!p || !what || !dst) return SEL_EINVAL;
+  if (!strncmp(what, "batch_", 6)) {     // k_batch dumps of the last batch launch
+    if (!p->bdump.hist || p->last_batch_nf < 1 || p->last_batch_nf > p->bdump_cap) return SEL_EINVAL;
+    const uint64_t nf = (uint64_t)p->last_batch_nf;
+    const uint64_t np = (uint64_t)batch_ntasks(p->geo, p->tl[0], p->bs) * batch_parts_per_task(p->geo);
+    const void *bsrc = nullptr;
+    uint64_t bneed = 0;
+    if (!strcmp(what, "batch_hist")) { bsrc = p->bdump.hist; bneed = nf * kNSlots * 4; }
+    else if (!strcmp(what, "batch_part")) { bsrc = p->bdump.part; bneed = nf * np * sizeof(Partial); }
+    else return SEL_EINVAL;
+    if (bytes != bneed) return SEL_EINVAL;
+    CK(cudaMemcpy(dst, bsrc, bneed, cudaMemcpyDeviceToHost));
+    return SEL_OK;
+  }
+  if (!p->dbg_mem) return SEL_EINVAL;
   const uint64_t N = (uint64_t)p->geo.N, B = (uint64_t)p->geo.n_pb, S = (uint64_t)p->size;
   const void *src = nullptr;
   uint64_t need = 0;
@@ -675,6 +767,20 @@ int sel_kernel_times(sel_plan_t p, double ms[3], uint64_t launches[3], int reset
   if (!p || !ms || !launches) return SEL_EINVAL;
   for (int k = 0; k < 3; ++k) { ms[k] = p->ms[k]; launches[k] = p->tcount[k]; }
   if (reset) for (int k = 0; k < 3; ++k) { p->ms[k] = 0; p->tcount[k] = 0; }
+  return SEL_OK;
+}
+
+int sel_batch_layout(sel_plan_t p, int64_t out[8]) {
+  if (!p || !out) return SEL_EINVAL;
+  const bool sampled = p->geo.s[0] > 1 || p->geo.s[1] > 1 || p->geo.s[2] > 1;
+  out[0] = batch_ntasks(p->geo, p->tl[0], p->bs);
+  out[1] = batch_parts_per_task(p->geo);
+  out[2] = batch_rows_per_part(p->geo);           // block rows per part (tile tasks)
+  out[3] = out[1] * out[2];                       // block rows per tile
+  out[4] = p->tl[0].tg.ntk;
+  out[5] = p->tl[0].tg.ntj;
+  out[6] = sampled ? 1 : 0;
+  out[7] = p->last_batch_G;
   return SEL_OK;
 }
 
@@ -709,6 +815,8 @@ void sel_plan_destroy(sel_plan_t p) {
   for (auto e : p->ev_k3) cudaEventDestroy(e);
   if (p->d_params) cudaFree(p->d_params);
   if (p->bstate) cudaFree(p->bstate);
+  if (p->bdump.hist) cudaFree(p->bdump.hist);
+  if (p->bdump.part) cudaFree(p->bdump.part);
   if (p->btab.d) cudaFree(p->btab.d);
   for (auto e : p->bev)
     if (e) cudaEventDestroy(e);

@@ -63,7 +63,7 @@ __device__ __forceinline__ unsigned int float_key(float v) {
 __device__ __forceinline__ float key_float(unsigned int k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
-struct FPart { double acc, err; unsigned long long bits, ovf; };
+struct FPart { double acc, err; unsigned long long bits, ovf, cnt; };
 
 struct BatchArgs {
   const CUtensorMap *tmaps;       // [nf], 64-B aligned, global
@@ -94,6 +94,8 @@ struct BatchArgs {
   FPart *fpart;                   // [G * kRing][kFinTasks]
   unsigned int *task_ctr;         // [G]
   sel_result *results;            // [nf]
+  unsigned int *hdump;            // optional [nf][kNSlots]: each field's histogram as the F tasks read it
+  Partial *pdump;                 // optional [nf][nT * CW]: each field's per-(task, warp) partials
   unsigned long long *prof;       // optional [gridDim * 8] cycle counters (warp 0 of each CTA)
 };
 
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   int4 *const stage_desc = reinterpret_cast<int4 *>(empty_bar + Cfg::STAGES);
   int4 *const stage_tile = stage_desc + Cfg::STAGES;
   __shared__ double s_red[3][CW];
-  __shared__ unsigned long long s_redu[2][CW];
+  __shared__ unsigned long long s_redu[3][CW];
   constexpr int NCHUNK = Cfg::W / kChunk;
   __shared__ int s_chunk[NCHUNK];                // window chunks with a nonzero bin (flush)
   __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2];
@@ -644,7 +646,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       constexpr int PER = kNSlots / kFinTasks;
       constexpr int NIT = (PER + NC - 1) / NC;
       double acc = 0.0;
-      unsigned long long novf = 0;
+      unsigned long long novf = 0, hcnt = 0;
       // every load first (one L2 round trip instead of one per bin), then the bins in the
       // same order as before (the per-thread sum order, hence the result, is unchanged)
       unsigned int cv[NIT];
@@ -655,12 +657,14 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       for (int k = 0; k < NIT; ++k) {
         const int s = id * PER + tid + k * NC;
         const unsigned int c = cv[k];
+        hcnt += c;
         if (c) {
           const double cd = (double)c;
           acc += cd * (lN - log2(cd));
           gh[s] = 0u;
         }
         if (s == kOvfSlot && tid + k * NC < PER) novf = c;
+        if (a.hdump && tid + k * NC < PER) a.hdump[(size_t)f * kNSlots + s] = c;   // test dump
       }
       const int np = a.nT * CW;
       const int per = (np + kFinTasks - 1) / kFinTasks;
@@ -670,6 +674,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       for (int t = p0 + tid; t < p1; t += NC) {
         bits += __ldcg(&tpf[t].bits);
         err += __ldcg(&tpf[t].err);
+        if (a.pdump) a.pdump[(size_t)f * np + t] = tpf[t];   // test dump
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -677,29 +682,37 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         err += __shfl_down_sync(0xffffffffu, err, o);
         bits += __shfl_down_sync(0xffffffffu, bits, o);
         novf += __shfl_down_sync(0xffffffffu, novf, o);
+        hcnt += __shfl_down_sync(0xffffffffu, hcnt, o);
       }
       consumer_sync<NC>();
-      if (lane == 0) { s_red[0][warp] = acc; s_red[1][warp] = err; s_redu[0][warp] = bits; s_redu[1][warp] = novf; }
+      if (lane == 0) {
+        s_red[0][warp] = acc; s_red[1][warp] = err;
+        s_redu[0][warp] = bits; s_redu[1][warp] = novf; s_redu[2][warp] = hcnt;
+      }
       consumer_sync<NC>();
       if (tid == 0) {
-        for (int w = 1; w < CW; ++w) { acc += s_red[0][w]; err += s_red[1][w]; bits += s_redu[0][w]; novf += s_redu[1][w]; }
+        for (int w = 1; w < CW; ++w) {
+          acc += s_red[0][w]; err += s_red[1][w];
+          bits += s_redu[0][w]; novf += s_redu[1][w]; hcnt += s_redu[2][w];
+        }
         FPart fp;
-        fp.acc = acc; fp.err = err; fp.bits = bits; fp.ovf = novf;
+        fp.acc = acc; fp.err = err; fp.bits = bits; fp.ovf = novf; fp.cnt = hcnt;
         fpf[id] = fp;
         fence_acq_rel_gpu();
         if (atomicAdd(a.fdone + f, 1u) == (unsigned)kFinTasks - 1) {   // last: result f
           fence_acq_rel_gpu();
           double S = 0.0, errs = 0.0;
-          unsigned long long tb = 0, ov = 0;
+          unsigned long long tb = 0, ov = 0, hc = 0;
           for (int k = 0; k < kFinTasks; ++k) {
             S += __ldcg(&fpf[k].acc);
             errs += __ldcg(&fpf[k].err);
             tb += __ldcg(&fpf[k].bits);
             ov += __ldcg(&fpf[k].ovf);
+            hc += __ldcg(&fpf[k].cnt);
           }
           const Params prm = a.params[f];
           const double mse = errs / (double)a.fa.n_values;
-          a.results[f] = assemble_result(prm, S, errs, tb, ov, a.fa, log10(prm.vr / prm.eb_abs),
+          a.results[f] = assemble_result(prm, S, errs, tb, ov, hc, a.fa, log10(prm.vr / prm.eb_abs),
                                          log10(prm.vr), mse > 0.0 ? log10(mse) : 0.0);
           fence_acq_rel_gpu();
           st_release(a.fin_ready + f, 1u);
@@ -744,6 +757,15 @@ int batch_sizes(const Geo &g, BatchSizes *bs) {
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs->smem) != cudaSuccess)
     return SEL_ECUDA;
   return SEL_OK;
+}
+
+int batch_parts_per_task(const Geo &g) { return g.ndims == 3 ? TileCfg<3>::CW : TileCfg<2>::CW; }
+int batch_rows_per_part(const Geo &g) { return g.ndims == 3 ? TileCfg<3>::BR : TileCfg<2>::BR; }
+
+bool batch_fits(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, int nf) {
+  if (tl.tg.ntk >= (1 << 16) || tl.tg.ntj >= (1 << 16)) return false;
+  const long long phase = kFinTasks + bs.nR + batch_ntasks(g, tl, bs);
+  return (long long)nf * phase < (1LL << 31);
 }
 
 // T tasks per field: TMA tiles, or (strides > 1) groups of one processed block per lane
@@ -791,9 +813,9 @@ static void build_group_sequence(int nfl, int nR, int nT, int lagT, int lagF, co
 
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
-                 sel_result *d_results, int sm_count, int G, int lagT, BatchTable *tab, cudaStream_t st,
-                 cudaEvent_t *ev) {
-  if (!tab || tl.tg.ntk >= (1 << 16) || tl.tg.ntj >= (1 << 16)) return SEL_EINVAL;
+                 sel_result *d_results, int sm_count, int G, int lagT, BatchTable *tab,
+                 const BatchDump &dump, cudaStream_t st, cudaEvent_t *ev) {
+  if (!tab || !batch_fits(g, tl, bs, nf)) return SEL_EINVAL;
   if (G < 1 || G > nf || G > sm_count || lagT < 1 || lagT > 4) return SEL_EINVAL;
   // state layout (device): tmaps | xs | params | counters | hist x2 | tpart x2 | fpart x2
   char *b = (char *)state;
@@ -824,12 +846,13 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   else
     for (int f = 0; f < nf; ++f)
       if (make_tile_map(&h_maps[f], d_fields[f], g)) return SEL_ECUDA;
+  // The histogram ring is zeroed when the state is allocated (sel_api.cu) and stays zero:
+  // the F tasks re-zero every nonzero bin they read, and every field is finalized.
   if (cudaMemcpyAsync(tmaps, h_maps.data(), sizeof(CUtensorMap) * nf, cudaMemcpyHostToDevice, st) !=
           cudaSuccess ||
       cudaMemcpyAsync(xs, d_fields, sizeof(float *) * nf, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemsetAsync(ctrs, 0, sizeof(unsigned int) * nctr, st) != cudaSuccess ||
-      cudaMemsetAsync(ctrs + 6 * (size_t)nf, 0xff, sizeof(unsigned int) * nf, st) != cudaSuccess ||
-      cudaMemsetAsync(hst, 0, (size_t)kH32Stride * 4 * nslot, st) != cudaSuccess)
+      cudaMemsetAsync(ctrs + 6 * (size_t)nf, 0xff, sizeof(unsigned int) * nf, st) != cudaSuccess)
     return SEL_ECUDA;
   BatchArgs a;
   a.tmaps = tmaps;
@@ -885,6 +908,8 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   a.tpart = tp;
   a.fpart = fp;
   a.results = d_results;
+  a.hdump = dump.hist;
+  a.pdump = dump.part;
   a.prof = g_batch_prof;
   const void *fn = g.ndims == 3 ? batch_fn<3>() : batch_fn<2>();
   void *args[] = {(void *)&a};

@@ -308,7 +308,7 @@ __device__ __forceinline__ void load_row(const float *__restrict__ x, const Geo 
 // P:410) and the Alg. 1 lines 7-10 selection (reading R16).
 // S = sum_s c_s log2(N/c_s); lg_* are log10(VR/eb), log10(VR), log10(MSE).
 __device__ __forceinline__ sel_result assemble_result(const Params &prm, double S, double errs,
-                                                      uint64_t tb, uint64_t novf,
+                                                      uint64_t tb, uint64_t novf, uint64_t hcnt,
                                                       const FinalizeArgs &fa, double lg_vr_eb,
                                                       double lg_vr, double lg_mse) {
   sel_result r = {};
@@ -320,6 +320,8 @@ __device__ __forceinline__ sel_result assemble_result(const Params &prm, double 
   r.n_sz_points = fa.n_sz;
   r.n_values = fa.n_values;
   r.n_blocks = fa.n_blocks;
+  r.hist_total = hcnt;
+  r.hist_ovf = novf;
   if (r.status == SEL_OK && fa.n_sz == 0) r.status = SEL_EDEGENERATE;   // single-value field
   if (r.status != SEL_OK) return r;
   const double Nsz = (double)fa.n_sz;

@@ -103,7 +103,7 @@ struct Workspace {
   double *fin_part;           // [kFinCTAs]
   double *fin_err;            // [kFinCTAs]
   unsigned long long *fin_bits; // [kFinCTAs]
-  unsigned long long *fin_ovf;// [1]
+  unsigned long long *fin_ovf;// [2]: overflow count, histogram total (device-counted)
   unsigned int *tickets;      // [2] last-block-done counters (minmax, finalize)
 };
 
@@ -139,14 +139,25 @@ struct BatchTable {
   long long key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
 };
 
+// optional k_batch test dumps (option "batch_debug"): per field, the histogram the F
+// tasks read and the per-(task, part) partials
+struct BatchDump {
+  unsigned int *hist = nullptr;   // [nf][kNSlots]
+  Partial *part = nullptr;        // [nf][nT * parts per task]
+};
+
 bool tile_supported(const Geo &g);
+// k_batch limits: 16-bit tile coordinates in the task table, 32-bit task indices
+bool batch_fits(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, int nf);
+int batch_parts_per_task(const Geo &g);
+int batch_rows_per_part(const Geo &g);
 int batch_sizes(const Geo &g, BatchSizes *bs);
 size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G);
 int batch_ntasks(const Geo &g, const TileLaunch &tl, const BatchSizes &bs);
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
                  sel_result *d_results, int sm_count, int G, int lagT, BatchTable *tab,
-                 cudaStream_t st, cudaEvent_t *ev);
+                 const BatchDump &dump, cudaStream_t st, cudaEvent_t *ev);
 int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl);
 int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Workspace &ws,
                 const DebugPtrs *dbg, cudaStream_t st);

@@ -459,6 +459,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
   const double Nsz = (double)fa.n_sz;
   const double lN = log2(Nsz);
   double acc = 0.0;
+  unsigned long long hcnt = 0;                       // device count of the slice's codes
   constexpr int PER = kNSlots / kFinCTAs;            // 1024 slots per CTA
   constexpr int SPT = PER / kFinThreads;             // slots per thread, all loads in flight
   unsigned long long cs[SPT];
@@ -468,6 +469,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
   for (int k = 0; k < SPT; ++k) {
     const int s = blockIdx.x * PER + k * kFinThreads + threadIdx.x;
     const unsigned long long c = cs[k];
+    hcnt += c;
     if (c) {
       const double cd = (double)c;
       acc += cd * (lN - log2(cd));          // c log2(N/c): exactly 0 for a single slot
@@ -493,7 +495,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
     acc += __shfl_down_sync(0xffffffffu, acc, o);
     err += __shfl_down_sync(0xffffffffu, err, o);
     bits += __shfl_down_sync(0xffffffffu, bits, o);
+    hcnt += __shfl_down_sync(0xffffffffu, hcnt, o);
   }
+  if ((threadIdx.x & 31) == 0 && hcnt) atomicAdd(ws.fin_ovf + 1, hcnt);   // exact integer total
   __shared__ double sacc[kFinThreads / 32], serr[kFinThreads / 32];
   __shared__ uint64_t sbits[kFinThreads / 32];
   __shared__ bool last;
@@ -542,7 +546,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Workspace ws, Finalize
 
   const double S = sfin[0] + sfin[2];
   const uint64_t tb = sfb[0] + sfb[1];
-  sel_result r = assemble_result(prm, S, errs, tb, __ldcg(ws.fin_ovf), fa, slog[0], slog[1], slog[2]);
+  const uint64_t hc = __ldcg(ws.fin_ovf + 1);
+  ws.fin_ovf[1] = 0ull;
+  sel_result r = assemble_result(prm, S, errs, tb, __ldcg(ws.fin_ovf), hc, fa, slog[0], slog[1], slog[2]);
   *out = r;
 }
 

@@ -42,9 +42,24 @@ def test_library_is_sm100a(sel):
     assert "sm_100a" in out
 
 
-def test_result_struct_layout(sel):
-    # 4 doubles, 2 int32, 7 doubles, 4 u64, 1 double, int32, float, int32, int32
-    assert __import__("ctypes").sizeof(sel.Result) == 4 * 8 + 8 + 7 * 8 + 4 * 8 + 8 + 16
+def test_result_struct_layout(sel, tmp_path):
+    """The ctypes mirror has the C struct's size and every member's offset (gcc on
+    include/sel.h)."""
+    import ctypes
+    names = [k for k, _ in sel.Result._fields_]
+    src = "#include <stdio.h>\n#include <stddef.h>\n#include \"sel.h\"\nint main(void){\n"
+    src += 'printf("%zu\\n", sizeof(sel_result));\n'
+    for k in names:
+        src += f'printf("%zu\\n", offsetof(sel_result, {k}));\n'
+    src += "return 0;}\n"
+    c = tmp_path / "layout.c"
+    c.write_text(src)
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
+    vals = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    assert vals[0] == ctypes.sizeof(sel.Result)
+    for k, off in zip(names, vals[1:]):
+        assert getattr(sel.Result, k).offset == off, k
 
 
 def test_strerror(sel):

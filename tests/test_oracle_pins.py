@@ -403,6 +403,67 @@ def test_gt_constant_block_closed_form(orc):
         assert orc.gt_count(u, kmin) == 34 + F - 2 * kmin
 
 
+# --------------------------------------------- per-block header (A13, whole field)
+@pytest.mark.parametrize("shape,kmin", [((8,), 17), ((8, 8), 15), ((8, 8, 8), 13)])
+def test_header_constant_field_through_estimate(orc, shape, kmin):
+    """The ZFP per-block header through the whole-field estimate (orc_estimate, not the
+    gt_count helper): a constant field x = 1.0 gives emax = 1, i = 2^29 and, after the
+    lift, the words (DC', 0, ..., 0) with DC' = negabinary(2^29) = 2^30 + 2^29 (digits 30
+    and 29: (-2)^30 + (-2)^29 = 2^29), so F = 30.  With eb_abs = 2^-10 (minexp -10) the
+    precision is p = 1 + 10 + 2(d+1), kmin = 32 - p, and every block costs
+    header 9 + (34 + F - 2 kmin) bits ((31-F) negative tests, 3 bits at
+    plane F, 2 per plane below).  A wrong header constant or cut rule fails this."""
+    nd = len(shape)
+    assert kmin == 32 - (1 + 10 + 2 * (nd + 1))
+    x = np.ones(shape, np.float32)
+    r = orc.estimate(x, 2.0 ** -10, mode="abs")
+    nblocks = int(np.prod([n // 4 for n in shape]))
+    per_block = 9 + 34 + 30 - 2 * kmin
+    assert r["zfp_total_bits"] == nblocks * per_block
+    assert r["n_blocks"] == nblocks
+
+
+@pytest.mark.parametrize("shape", [(8,), (8, 8), (8, 8, 8)])
+def test_header_precision_zero_block_costs_one_bit(orc, shape):
+    """p = 0 (eb far above the block's magnitude, P:436 'maximum bit-plane determined by
+    the error bound'): the block is a single header bit and its whole content is the error.
+    Constant 1.0 field, eb_abs = 2^40: bits = 1 per block; the DC coefficient 2^29 is
+    dropped, E_b = w_0 (2^29)^2 2^(2(1-30)) = 4^d (the block's squared-error sum), so
+    MSE = 1.0 exactly -- the error of reconstructing 1.0 as 0."""
+    x = np.ones(shape, np.float32)
+    r = orc.estimate(x, 2.0 ** 40, mode="abs")
+    nblocks = int(np.prod([n // 4 for n in shape]))
+    assert r["zfp_total_bits"] == nblocks
+    assert r["zfp_mse"] == 1.0
+
+
+def test_header_golden_hand_count(orc):
+    """tests/golden/gt_hand_1d.json: 42 EC bits + the 9-bit header = 51."""
+    g = gold("gt_hand_1d.json")
+    assert orc.gt_count(g["u"], g["kmin"]) + 9 == g["block_bits_with_header"] == 51
+
+
+# -------------------------------------------- threaded oracle (bit-identical)
+@pytest.mark.parametrize("shape,stride", [((37, 45, 70), None), ((203, 517), (1, 10)),
+                                          ((1001,), None), ((20, 24, 36), (2, 1, 3))])
+def test_threaded_oracle_is_bit_identical(orc, shape, stride):
+    """orc_estimate_mt (slabs of blocks per thread, exact merges, E_b summed in block
+    order) returns the single-threaded result bit for bit, dumps included."""
+    rng = np.random.default_rng(sum(shape))
+    x = np.cumsum(rng.standard_normal(shape), axis=-1).astype(np.float32)
+    a = orc.estimate(x, 1e-4, stride=stride, debug=True, threads=1)
+    for t in (2, 3, 7):
+        b = orc.estimate(x, 1e-4, stride=stride, debug=True, threads=t)
+        for k in a:
+            if k == "debug":
+                for kk in a[k]:
+                    assert np.array_equal(a[k][kk], b[k][kk]), (t, kk)
+            else:
+                assert a[k] == b[k] or (a[k] != a[k] and b[k] != b[k]), (t, k)
+    assert a["hist_total"] == a["n_sz_points"] == int(a["debug"]["hist"].sum())
+    assert a["hist_ovf"] == int(a["debug"]["hist"][65535])
+
+
 # ---------------------------------------------------------- error (A14)
 def test_gain_weights_are_inverse_column_norms(orc):
     cn = [sum(AINV[r][c] ** 2 for r in range(4)) for c in range(4)]

@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 
 REL = 1e-6
 EXACT_KEYS = ("n_sz_points", "n_values", "n_blocks", "zfp_total_bits", "minexp", "r_f", "choice_eb",
-              "choice", "matched", "value_range", "eb_abs")
+              "choice", "matched", "value_range", "eb_abs", "hist_total", "hist_ovf")
 CLOSE_KEYS = ("sz_entropy", "sz_bits_per_value", "sz_psnr", "zfp_bits_per_value", "zfp_psnr",
               "zfp_mse", "zfp_err_sum", "sz_bits_matched", "sz_eb_matched", "sz_overflow_frac")
 
@@ -31,10 +31,22 @@ def sel():
     return sel
 
 
-def close(a, b, rel=REL, abs_=1e-12):
+def close(a, b, rel=REL, abs_=0.0):
+    """|a - b| <= rel * max(|a|, |b|): relative only (0 == 0 passes; no absolute floor,
+    so tiny MSEs of small-scale fields are compared at full relative precision)."""
     if isinstance(a, float) and (math.isinf(a) or math.isinf(b)):
         return a == b
     return abs(a - b) <= max(rel * max(abs(a), abs(b)), abs_)
+
+
+NEAR_TIE = 1e-9
+
+
+def tie_margin(r) -> float:
+    """Relative margin of Alg. 1 line 10's comparison, |BR_sz* - BR_zfp| / BR_zfp (SURVEY
+    8(c) A16(iv)): a flip between two implementations needs a margin near 1e-12."""
+    a, b = float(r["sz_bits_matched"]), float(r["zfp_bits_per_value"])
+    return abs(a - b) / max(abs(a), abs(b), 1e-300)
 
 
 def compare_scalars(g, o, tag=""):
@@ -43,6 +55,7 @@ def compare_scalars(g, o, tag=""):
     for k in CLOSE_KEYS:
         assert close(float(g[k]), float(o[k])), (tag, k, g[k], o[k])
     assert g["status"] == 0
+    assert g["hist_total"] == g["n_sz_points"], tag       # no code lost or duplicated
 
 
 def run_gpu(sel, x, eb, mode="rel", stride=None, debug=False, offset_elems=0):
@@ -374,6 +387,94 @@ def test_kernel_timing_option(sel):
     assert n == [3, 3, 3] and all(m > 0 for m in ms)
 
 
+# ---------------------------------------------------------------- k_batch element-exact
+def _part_sums(vals, lay, grid_shape, stride_all_one):
+    """Sum per-block values (processed-block row-major order) over k_batch's parts."""
+    ppt, rpp, rpt = lay["parts_per_task"], lay["rows_per_part"], lay["rows_per_tile"]
+    nT = lay["n_tasks"]
+    if lay["sampled"]:
+        v = np.zeros(nT * ppt * 32, vals.dtype)
+        v[: vals.size] = vals
+        return v.reshape(nT * ppt, 32).sum(axis=1)
+    nb0, nb1, nb2 = grid_shape
+    ntj, ntk = lay["ntj"], lay["ntk"]
+    g = np.zeros((nb0, ntj * rpt, ntk * 32), vals.dtype)
+    g[:, :nb1, :nb2] = vals.reshape(nb0, nb1, nb2)
+    g = g.reshape(nb0, ntj, ppt, rpp, ntk, 32).sum(axis=(3, 5))      # (bi, btj, p, btk)
+    return g.transpose(0, 1, 3, 2).reshape(-1)                      # task (bi, btj, btk), part p
+
+
+def check_batch_exact(sel, orc, xs, eb, stride=None, tag="", threads=0):
+    """The benched kernel (k_batch, one launch for the stack, bench launch configuration)
+    against the oracle ELEMENT BY ELEMENT: every field's 65,536-bin histogram bin-exact,
+    the device-counted histogram total / overflow exact, every per-(task, part) ZFP
+    partial's bit count exact and error to 1e-12, and the scalars (1e-6 / exact)."""
+    shape = xs[0].shape
+    ts = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in xs]
+    with sel.Plan(shape, eb, "rel", stride) as p:
+        plain = p.estimate_batch(ts)                     # no dumps: what bench.py times
+        l0 = p.launch_count
+        p.set_option("batch_debug", 1)
+        out = p.estimate_batch(ts)
+        assert p.launch_count - l0 == 1, "k_batch did not run"
+        hist = p.batch_debug_copy("hist", len(xs))
+        part = p.batch_debug_copy("part", len(xs))
+        lay = p.batch_layout()
+    assert out == plain, tag                              # the dumps change nothing
+    nd = len(shape)
+    grid = [1] * (3 - nd) + [(n + 3) // 4 for n in shape]
+    ties = 0
+    res = []
+    for i, x in enumerate(xs):
+        o = orc.estimate(x, eb, mode="rel", stride=stride, debug=("hist", "bits", "err"),
+                         threads=threads)
+        t = f"{tag}/{i}"
+        compare_scalars(out[i], o, t)
+        od = o["debug"]
+        assert np.array_equal(hist[i].astype(np.uint64), od["hist"]), (t, "histogram")
+        pb = _part_sums(od["bits"].astype(np.uint64), lay, grid, stride is None)
+        assert np.array_equal(part[i]["bits"], pb), (t, "part bits")
+        pe = _part_sums(od["err"], lay, grid, stride is None)
+        assert np.allclose(part[i]["err"], pe, rtol=1e-12, atol=0), (t, "part err")
+        ties += tie_margin(out[i]) < NEAR_TIE
+        res.append((out[i], o))
+    assert ties == 0, (tag, "near ties", ties)
+    return res
+
+
+@pytest.mark.parametrize("shape,stride", [((64, 256), None), ((203, 516), None), ((40, 300), (1, 10)),
+                                          ((16, 40, 132), None), ((37, 45, 68), None),
+                                          ((20, 24, 36), (2, 1, 3))])
+def test_batch_exact_small(sel, orc, shape, stride):
+    """k_batch element-exact on small ragged stacks (several tiles, partial tiles)."""
+    import synth
+    if len(shape) == 2:
+        xs = [synth.c2_field(i, shape=shape) for i in range(4)]
+    else:
+        xs = [synth.c3_field(i, shape=shape) for i in (0, 5, 9)]
+    check_batch_exact(sel, orc, xs, 1e-4, stride, tag=f"bx{shape}{stride}")
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (16, 16, 64)])
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_batch_kernel_nonfinite(sel, shape, bad):
+    """NaN / +Inf / -Inf through k_batch (aligned, tile path): SEL_ENONFINITE for that field
+    only, single-field and in a stack."""
+    rng = np.random.default_rng(1)
+    good = rng.standard_normal(shape).astype(np.float32)
+    x = good.copy()
+    x.flat[x.size // 3] = bad
+    tg, tx = torch.from_numpy(good).cuda(), torch.from_numpy(x).cuda()
+    with sel.Plan(shape, 1e-3) as p:
+        l0 = p.launch_count
+        with pytest.raises(sel.SelError) as e:
+            p.estimate(tx)
+        assert e.value.status == sel.SEL_ENONFINITE
+        assert p.launch_count - l0 == 1                   # it was k_batch
+        out = p.estimate_batch([tg, tx, tg])
+    assert out[1]["status"] == sel.SEL_ENONFINITE and out[0]["status"] == 0 and out[2]["status"] == 0
+
+
 # ---------------------------------------------------------------- full sizes
 def _padded_block(x, b, nd):
     sl = []
@@ -421,60 +522,61 @@ def _sampled_block_check(orc, x, g, dbg, stride, nblocks=400, seed=0):
             assert dbg["codes"][idx] == orc.quantize(orc.lorenzo(x, idx), r_f), idx
 
 
-def _full_size_check(sel, orc, x, eb, stride=None, full_oracle=True, tag=""):
-    nd = x.ndim
-    st = stride or (1,) * nd
+def _per_field_debug_check(sel, orc, x, eb, stride=None, tag=""):
+    """Intermediates (codes, emax, coefficients, words, bits, errors) of the per-field
+    debug kernels on sampled blocks of a full-size field."""
+    st = stride or (1,) * x.ndim
     t = torch.from_numpy(x).cuda()
     with sel.Plan(x.shape, eb, "rel", stride) as p:
-        g = p.estimate(t)                                 # bench launch configuration
+        g = p.estimate(t)
         p.set_option("debug", 1)
         gd = p.estimate(t)
         dbg = {k: p.debug_copy(k) for k in ("codes", "hist", "emax", "coef", "uword", "bits", "err")}
-    for k in g:      # debug build may use another grid: double sums agree to rounding
+    for k in g:
         if isinstance(g[k], float):
             assert close(g[k], gd[k], rel=1e-12), (tag, k)
         else:
             assert g[k] == gd[k], (tag, k)
-    # properties at any size
     assert int(dbg["hist"].sum()) == g["n_sz_points"]
     assert int(dbg["bits"].astype(np.uint64).sum()) == g["zfp_total_bits"]
-    assert close(float(dbg["err"].sum()), g["zfp_err_sum"], rel=1e-9)
-    assert g["value_range"] == float(x.max()) - float(x.min())
-    # oracle's entropy of the GPU histogram (K3 at full size)
-    assert close(orc.entropy(dbg["hist"]), g["sz_entropy"])
     _sampled_block_check(orc, x, g, dbg, st)
-    if full_oracle:
-        o = orc.estimate(x, eb, mode="rel", stride=stride)
-        compare_scalars(g, o, tag)
-    return g
 
 
 def test_full_config2_fields(sel, orc):
+    """C2 at full size: 20 fields (both kinds: 0 and 10 are piecewise-constant), every
+    block and every 10th block column, element-exact through k_batch."""
     import synth
-    for i in (0, 7):
-        x = synth.c2_field(i)
-        _full_size_check(sel, orc, x, 1e-4, tag=f"C2full{i}")
-        _full_size_check(sel, orc, x, 1e-4, stride=(1, 10), tag=f"C2s{i}")
+    xs = [synth.c2_field(i) for i in range(20)]
+    check_batch_exact(sel, orc, xs, 1e-4, tag="C2full")
+    check_batch_exact(sel, orc, xs, 1e-4, stride=(1, 10), tag="C2s")
+    _per_field_debug_check(sel, orc, xs[0], 1e-4, tag="C2dbg")
 
 
-def test_full_config3_field(sel, orc):
+@pytest.mark.parametrize("eb", [1e-3, 1e-4, 1e-5])
+def test_full_config3_fields(sel, orc, eb):
+    """C3 at full size: all 13 fields at every eb, element-exact through k_batch."""
     import synth
-    x = synth.c3_field(5)                 # zero-heavy
-    for eb in (1e-3, 1e-5):
-        _full_size_check(sel, orc, x, eb, tag=f"C3full/{eb}")
+    xs = [synth.c3_field(i) for i in range(13)]
+    check_batch_exact(sel, orc, xs, eb, tag=f"C3full/{eb}")
+    if eb == 1e-5:
+        _per_field_debug_check(sel, orc, xs[5], eb, tag="C3dbg")
 
 
-def test_full_config4_field(sel, orc):
+def test_full_config4_fields(sel, orc):
+    """C4 at full size: all 6 fields, every block and 1/64 of the blocks."""
     import synth
-    x = synth.c4_field(0)                 # heavy-tailed lognormal, VR ~ 1e6
-    _full_size_check(sel, orc, x, 1e-4, stride=(4, 4, 4), tag="C4s")
-    _full_size_check(sel, orc, x, 1e-4, full_oracle=True, tag="C4full")
+    xs = [synth.c4_field(i) for i in range(6)]
+    check_batch_exact(sel, orc, xs, 1e-4, tag="C4full")
+    check_batch_exact(sel, orc, xs, 1e-4, stride=(4, 4, 4), tag="C4s")
 
 
-@pytest.mark.parametrize("mix,eb", [(2, 1e-6), (1, 1e-3)])
-def test_full_config5_field(sel, orc, mix, eb):
+@pytest.mark.parametrize("mix", [0, 1, 2])
+def test_full_config5_fields(sel, orc, mix):
+    """C5 at full size (1024^3, 4 GiB): every eb of the sweep, element-exact through
+    k_batch against the (threaded, bit-identical) oracle."""
     import synth
     x = synth.c5_field(mix)
-    g = _full_size_check(sel, orc, x, eb, full_oracle=False, tag=f"C5full{mix}")
-    if mix == 2:
-        assert g["sz_overflow_frac"] > 0.5
+    for eb in synth.CONFIGS[5]["eb_rel"]:
+        (g, o), = check_batch_exact(sel, orc, [x], eb, tag=f"C5full{mix}/{eb}")
+        if mix == 2 and eb <= 1e-6:
+            assert g["sz_overflow_frac"] > 0.5
