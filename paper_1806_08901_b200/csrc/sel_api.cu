@@ -259,8 +259,7 @@ int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st,
     p->bstate_cap = 0;
     if (cudaMalloc(&p->bstate, need) != cudaSuccess) return SEL_ENOMEM;
     p->bstate_cap = need;
-    // zero once (the histogram ring stays zero between launches: the F tasks re-zero it)
-    CK(cudaMemsetAsync(p->bstate, 0, need, st));
+    p->btab.hist_clean = 0;          // launch_batch zeroes the histogram ring
   }
   BatchDump dump;
   if (p->batch_debug) {

@@ -828,13 +828,14 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   };
   const int nT = batch_ntasks(g, tl, bs);
   const bool sampled = g.s[0] > 1 || g.s[1] > 1 || g.s[2] > 1;
+  // the histogram ring first, at a fixed offset: its slots stay zero between launches
+  const size_t nslot = (size_t)G * kRing;
+  unsigned int *hst = (unsigned int *)take((size_t)kH32Stride * 4 * nslot);
   CUtensorMap *tmaps = (CUtensorMap *)take(sizeof(CUtensorMap) * nf, 128);
   const float **xs = (const float **)take(sizeof(float *) * nf);
   Params *params = (Params *)take(sizeof(Params) * nf);
   const size_t nctr = 8 * (size_t)nf + (size_t)G;
   unsigned int *ctrs = (unsigned int *)take(sizeof(unsigned int) * nctr);
-  const size_t nslot = (size_t)G * kRing;
-  unsigned int *hst = (unsigned int *)take((size_t)kH32Stride * 4 * nslot);
   Partial *tp = (Partial *)take(sizeof(Partial) * (size_t)nT * bs.cw * nslot);
   FPart *fp = (FPart *)take(sizeof(FPart) * kFinTasks * nslot);
   if (off > state_bytes) return SEL_EINVAL;
@@ -846,8 +847,13 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   else
     for (int f = 0; f < nf; ++f)
       if (make_tile_map(&h_maps[f], d_fields[f], g)) return SEL_ECUDA;
-  // The histogram ring is zeroed when the state is allocated (sel_api.cu) and stays zero:
-  // the F tasks re-zero every nonzero bin they read, and every field is finalized.
+  // The histogram ring stays zero between launches (the F tasks re-zero every nonzero bin
+  // they read, and every field is finalized); only slots not known to be zero -- a fresh
+  // state, or more groups than before (the ring grew into other state) -- are cleared.
+  if (tab->hist_clean < nslot) {
+    if (cudaMemsetAsync(hst, 0, (size_t)kH32Stride * 4 * nslot, st) != cudaSuccess) return SEL_ECUDA;
+  }
+  tab->hist_clean = nslot;
   if (cudaMemcpyAsync(tmaps, h_maps.data(), sizeof(CUtensorMap) * nf, cudaMemcpyHostToDevice, st) !=
           cudaSuccess ||
       cudaMemcpyAsync(xs, d_fields, sizeof(float *) * nf, cudaMemcpyHostToDevice, st) != cudaSuccess ||

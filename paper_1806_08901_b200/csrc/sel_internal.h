@@ -137,6 +137,7 @@ struct BatchTable {
   void *d = nullptr;
   size_t cap = 0;
   long long key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  size_t hist_clean = 0;   // leading histogram-ring slots of the batch state known to be zero
 };
 
 // optional k_batch test dumps (option "batch_debug"): per field, the histogram the F
