@@ -43,6 +43,9 @@ constexpr int kH32Stride = kNSlots + 4;
 #ifndef SEL_CLAIM
 #define SEL_CLAIM 1                            // producer: task ids claimed per atomic
 #endif
+#ifndef SEL_PBACKOFF
+#define SEL_PBACKOFF 64                        // producer: longest sleep between stage probes (ns)
+#endif
 #ifndef SEL_BATCH_PROF
 #define SEL_BATCH_PROF 0                       // 1: per-CTA cycle counters (sel_dev_batch_profile)
 #endif
@@ -181,6 +184,16 @@ __device__ __forceinline__ float fmin_nan(float a, float b) {   // NaN if either
   asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
   return r;
 }
+__device__ __forceinline__ float fmin3_nan(float a, float b, float c) {   // sm_100 FMNMX3
+  float r;
+  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __device__ __forceinline__ unsigned int ld_acquire_cta(const unsigned int *p) {
   unsigned int v;
   asm volatile("ld.acquire.cta.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -202,6 +215,16 @@ constexpr int kRelQ = 16;
 
 template <int D>
 constexpr int batch_threads() { return (TileCfg<D>::CW + 2) * 32; }   // + producer + release warp
+
+// producer: wait until a stage is free, sleeping with a short back-off (a tight probe
+// loop took ~7 % of the 3D kernel's issued instructions, ncu r01c)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
+  unsigned int ns = 64;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    if (ns < SEL_PBACKOFF) ns <<= 1;
+  }
+}
 
 // warp 0 lane 0 spins until *flag >= target (acquire); the caller syncs the consumers
 __device__ __forceinline__ void spin_until(const unsigned int *flag, unsigned int target) {
@@ -331,7 +354,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       long long pp_start = PCLOCK(), pp_wait = 0, pp_dec = 0, pp_n = 0;
       for (;;) {
         const long long pw0 = PCLOCK();
-        mbar_wait_sleep(&empty_bar[stage], ph ^ 1u);
+        mbar_wait_backoff(&empty_bar[stage], ph ^ 1u);
         PROF(pp_wait += clock64() - pw0; ++pp_n);
         stage_desc[stage] = make_int4(t0.kind, t0.f, t0.id, t0.phase);
         stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, t0.slot);
@@ -605,13 +628,18 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         const float4 *src = reinterpret_cast<const float4 *>(S);
         // min propagates NaN (min.NaN), so non-finite values show up in the reduced
         // min / max themselves: NaN -> mn is NaN, +-inf -> mx / mn infinite
-        float mn = INFINITY, mx = -INFINITY;
+        // 3-input min / max (sm_100 FMNMX3), two accumulator pairs to break the chains
+        float mn = INFINITY, mx = -INFINITY, mn2 = INFINITY, mx2 = -INFINITY;
 #pragma unroll 8
         for (int i = slot * 32 + lane; i < n4; i += kRWarps * 32) {
           const float4 q = src[i];
-          mn = fmin_nan(mn, fmin_nan(fmin_nan(q.x, q.y), fmin_nan(q.z, q.w)));
-          mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+          mn = fmin3_nan(mn, q.x, q.y);
+          mx = fmax3(mx, q.x, q.y);
+          mn2 = fmin3_nan(mn2, q.z, q.w);
+          mx2 = fmax3(mx2, q.z, q.w);
         }
+        mn = fmin_nan(mn, mn2);
+        mx = fmaxf(mx, mx2);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[stage]);
 #pragma unroll

@@ -147,9 +147,10 @@ __device__ __forceinline__ double pow2d(int k) {   // 2^k, k in [-1022, 1023]
   return __hiloint2double((1023 + k) << 20, 0);
 }
 
-// Error sum in double, coefficient by coefficient (used when kmin >= 30, incl. p == 0).
+// Error sum in double, coefficient by coefficient in sequency order (used when kmin >= 30,
+// incl. p == 0, where the squared errors no longer fit exact 64-bit class sums).
 template <int D>
-__device__ __forceinline__ double zfp_err_double(const uint32_t *u, int kmin, int emax) {
+__device__ __forceinline__ double zfp_err_double(const int (&cf)[Tab<D>::SIZE], int kmin, int emax) {
   constexpr int SZ = Tab<D>::SIZE;
   const uint32_t low = kmin >= 32 ? 0xffffffffu : ((1u << kmin) - 1u);
   const uint32_t Mk = 0xAAAAAAAAu & low;
@@ -158,7 +159,8 @@ __device__ __forceinline__ double zfp_err_double(const uint32_t *u, int kmin, in
     constexpr int j = decltype(J)::value;
     constexpr int n = Tab<D>::make_perm().v[j];
     constexpr double w = Tab<D>::gain(n);
-    const long long e = (long long)((u[j] & low) ^ Mk) - (long long)Mk;
+    const uint32_t uj = to_negabinary(cf[n]);
+    const long long e = (long long)((uj & low) ^ Mk) - (long long)Mk;
     const double ed = (double)e;
     E = __dadd_rn(E, __dmul_rn(w, __dmul_rn(ed, ed)));
   });
@@ -166,6 +168,9 @@ __device__ __forceinline__ double zfp_err_double(const uint32_t *u, int kmin, in
 }
 
 // One 4^d block: v (natural order, edge-replicated) -> EC bits and gain-weighted error.
+// The sequency-ordered negabinary words are formed on the fly in ONE descending pass that
+// does both the bit count and the error classes, so a lifted coefficient dies as soon as
+// it is consumed (register pressure: the 3D block is 64 words).
 template <int D, bool DBG>
 __device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int minexp,
                                           uint32_t &bits, double &E, int &emax,
@@ -213,66 +218,64 @@ __device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int mi
 #pragma unroll
     for (int l = 0; l < 16; ++l) fwd_lift(cf[l], cf[l + 16], cf[l + 32], cf[l + 48]);
   }
-  // sequency reorder + negabinary (R10, R11)
-  static_for<0, SZ>([&](auto J) {
-    constexpr int j = decltype(J)::value;
-    constexpr int n = Tab<D>::make_perm().v[j];
-    u[j] = to_negabinary(cf[n]);
-  });
   // fixed-accuracy cut (R12)
   int prec = emax - minexp + 2 * (D + 1);
   prec = prec < 0 ? 0 : (prec > 32 ? 32 : prec);
   const int kmin = 32 - prec;
-  if (prec == 0) {
-    bits = 1u;
-  } else {
-  // closed-form group-testing count (R13).  f_j = floor(log2 u_j) (-1 for 0),
-  // S_j = max_{j'>=j} f_j', Q_j = max(kmin-1, S_j):
+  // kmin >= 30 (incl. p == 0, where every plane is dropped): the error in double, first
+  double Ed = 0.0;
+  if (kmin >= 30) Ed = zfp_err_double<D>(cf, kmin, emax);
+  // ONE pass over the sequency order j = SZ-1 .. 0 (R10 reorder + R11 negabinary on the
+  // fly): the closed-form group-testing count (R13) and the exact error class sums (R14).
+  //   bit count: f_j = floor(log2 u_j) (-1 for 0), S_j = max_{j'>=j} f_j',
+  //   Q_j = max(kmin-1, S_j):
   //   GT = sum_j max(0, S_j-kmin+1)                = sum_j Q_j - SZ (kmin-1)
   //      + #{j : f_j >= kmin and f_j >= S_{j+1}}   (f_j >= kmin and f_j >= Q_{j+1})
   //      + 32 - max(f_L+1, kmin) - [f_L >= kmin]
-  // evaluated with R_j = max(kmin, S_j): the middle set is C = {j : f_j >= R_{j+1}}
-  // (a bit mask, counted by popc), and sum_j Q_j = sum_j R_j - z with z = #{j : S_j <
-  // kmin} = SZ-1-max(C) (the highest j of C is the last significant coefficient).
-    int R = kmin, sR = 0;
-    uint32_t cm0 = 0u, cm1 = 0u;   // C for j < 32 / j >= 32
-#pragma unroll
-    for (int j = SZ - 1; j >= 0; --j) {
-      const int f = flo(u[j]);
-      if (f >= R) {
-        if (j < 32) cm0 |= 1u << (j & 31);
-        else cm1 |= 1u << (j & 31);
-      }
-      R = max(R, f);
-      sR += R;
-    }
-    const int last = cm1 ? 32 + flo(cm1) : flo(cm0);       // -1 if C is empty
-    const int t1 = sR - (SZ - 1 - last);
-    const int t2 = __popc(cm0) + __popc(cm1);
-    const int fL = flo(u[SZ - 1]);
-    const int t3 = 32 - max(fL + 1, kmin) - (fL >= kmin ? 1 : 0);
-    bits = (uint32_t)(9 + t1 - SZ * (kmin - 1) + t2 + t3);
-  }
-  // gain-weighted truncation error (R14): e_j = value of the dropped negabinary digits
-  // = ((u & low) ^ M) - M; e_j^2 summed EXACTLY in 64-bit integers per weight class
-  // (|e| < 2^29 for kmin <= 29, so 64 terms fit), then weighted in double.  kmin >= 30
-  // (incl. p == 0, where every plane is dropped) takes the double path.
-  if (kmin >= 30) {
-    E = zfp_err_double<D>(u, kmin, emax);
-    return;
-  }
-  const uint32_t low = (1u << kmin) - 1u;
+  //   evaluated with R_j = max(kmin, S_j): the middle set is C = {j : f_j >= R_{j+1}}
+  //   (a bit mask, counted by popc), and sum_j Q_j = sum_j R_j - z with z = #{j : S_j <
+  //   kmin} = SZ-1-max(C) (the highest j of C is the last significant coefficient).
+  //   error: e_j = value of the dropped negabinary digits = ((u & low) ^ M) - M; e_j^2
+  //   summed EXACTLY in 64-bit integers per weight class (|e| < 2^29 for kmin <= 29, so
+  //   the class sums fit), then weighted in double.
+  const uint32_t low = (1u << (kmin & 31)) - 1u;   // (only used when kmin < 30)
   const uint32_t Mk = 0xAAAAAAAAu & low;
   unsigned long long acc[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = 0ull;
-  static_for<0, SZ>([&](auto J) {
-    constexpr int j = decltype(J)::value;
+  int R = kmin, sR = 0;
+  uint32_t cm0 = 0u, cm1 = 0u;   // C for j < 32 / j >= 32
+  int fL = -1;
+  static_for<0, SZ>([&](auto JJ) {
+    constexpr int j = SZ - 1 - decltype(JJ)::value;
     constexpr int n = Tab<D>::make_perm().v[j];
     constexpr int c = Tab<D>::cls_of(n);
-    const int e = (int)((u[j] & low) ^ Mk) - (int)Mk;
+    const uint32_t uj = to_negabinary(cf[n]);
+    if constexpr (DBG) u[j] = uj;
+    const int f = flo(uj);
+    if constexpr (j == SZ - 1) fL = f;
+    if (f >= R) {
+      if (j < 32) cm0 |= 1u << (j & 31);
+      else cm1 |= 1u << (j & 31);
+    }
+    R = max(R, f);
+    sR += R;
+    const int e = (int)((uj & low) ^ Mk) - (int)Mk;
     acc[c] += (unsigned long long)((long long)e * (long long)e);
   });
+  if (prec == 0) {
+    bits = 1u;
+  } else {
+    const int last = cm1 ? 32 + flo(cm1) : flo(cm0);       // -1 if C is empty
+    const int t1 = sR - (SZ - 1 - last);
+    const int t2 = __popc(cm0) + __popc(cm1);
+    const int t3 = 32 - max(fL + 1, kmin) - (fL >= kmin ? 1 : 0);
+    bits = (uint32_t)(9 + t1 - SZ * (kmin - 1) + t2 + t3);
+  }
+  if (kmin >= 30) {
+    E = Ed;
+    return;
+  }
   double s = 0.0;
   static_for<0, NC>([&](auto Cc) {
     constexpr int c = decltype(Cc)::value;
