@@ -337,6 +337,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the config's sampled-stride line")
+    ap.add_argument("--no-rd", action="store_true", help="skip the multi-eb (rate-distortion curve) line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -455,6 +456,32 @@ def main():
                "unit": "GB/s", "ms_per_step": ams}
         ap2.close()
 
+    # ---- the rate-distortion curve, three error bounds per field from ONE
+    # read (sel_estimate_multi, one call per field), same fields; value = GB/s of input,
+    # eb_estimates_gbs = k x that (the single-eb work it replaces)
+    rd = None
+    if not args.no_rd:
+        rd_ebs = [10 * eb, eb, eb / 10]
+        mp = sel.Plan(shape, eb, "rel", st)
+        for f in dfields[:2]:
+            mp.estimate_multi(f, rd_ebs)
+        torch.cuda.synchronize()
+        barrier(world)
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        rsteps = max(1, min(args.steps, 3))
+        r0.record(stream)
+        for _ in range(rsteps):
+            for f in dfields:
+                mp.estimate_multi(f, rd_ebs)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        rms = max_over_ranks(world, r0.elapsed_time(r1)) / rsteps
+        rv = world * field_bytes / (rms * 1e-3) / 1e9
+        rd = {"ebs_rel": rd_ebs, "value": rv, "unit": "GB/s", "eb_estimates_gbs": rv * len(rd_ebs),
+              "ms_per_step": rms, "entry": "sel_estimate_multi per field (k_minmax + k_multi + k finalizes)"}
+        mp.close()
+
     if rank != 0:
         barrier(world)
         return 0
@@ -500,7 +527,7 @@ def main():
                    "fields_per_s": fields_per_s,
                    "pct_of_hbm_peak": 100.0 * value / (peak * world),
                    "sz_chosen": n_sz, "zfp_chosen": nf - n_sz,
-                   "sampled_mode": alt},
+                   "sampled_mode": alt, "rd_curve": rd},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": names[dom],
                      "peak_source": peak_kind,

@@ -123,6 +123,20 @@ int sel_set_option(sel_plan_t plan, const char *key, double value);
  * Errors: SEL_EINVAL, SEL_ENONFINITE, SEL_EDEGENERATE, SEL_ECUDA. */
 int sel_estimate(sel_plan_t plan, const float *d_field, void *stream, sel_result *out);
 
+/* N1: the rate-distortion curve of one field at k error bounds from ONE read
+ * (P:384-392 -- rate-distortion compared over error bounds; Alg. 1 lines 2-10 per eb,
+ * P:478-490).  ebs[0..k) (1 <= k <= 8) replace the plan's eb, interpreted in the plan's
+ * mode (absolute, or x value range); dims, stride and block are the plan's.  The value
+ * range is computed once, every processed block is read once, its Lorenzo residuals and
+ * ZFP transform are formed once, and the eb-dependent stages (quantisation + histogram,
+ * fixed-accuracy cut, bit count, error) run per eb.  out[e] (host, k entries) equals what
+ * sel_estimate would return at ebs[e] (per-eb status in out[e].status: SEL_ENONFINITE,
+ * SEL_EDEGENERATE, ...).  d_field: device, float32, C order, not modified; the call
+ * synchronises `stream`.  Errors: SEL_EINVAL (NULL, k out of range, eb not finite or <= 0,
+ * option kernel_timing or debug set), SEL_ENOMEM, SEL_ECUDA. */
+int sel_estimate_multi(sel_plan_t plan, const float *d_field, int k, const double *ebs, void *stream,
+                       sel_result *out);
+
 /* Estimate n fields of the plan's shape (d_fields: HOST array of n DEVICE
  * pointers).  out[i].status holds each field's status; returns SEL_OK if the
  * launches succeeded (individual fields may still carry an error status). */

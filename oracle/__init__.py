@@ -161,6 +161,12 @@ def default_threads() -> int:
         return max(1, os.cpu_count() or 1)
 
 
+def estimate_multi(x: np.ndarray, ebs, mode: str = "rel", stride=None, threads: int = 1) -> list:
+    """SURVEY 8(f) N1 by its definition: the estimate of Alg. 1 lines 1-10 at every error
+    bound of the rate-distortion sweep, one plain estimate per eb."""
+    return [estimate(x, e, mode=mode, stride=stride, threads=threads) for e in ebs]
+
+
 def estimate(x: np.ndarray, eb: float, mode: str = "rel", stride=None, sz_offset: float = 0.5,
              debug: bool = False, threads: int = 1) -> dict:
     """Alg. 1 lines 1-10 on a C-order float32 field.

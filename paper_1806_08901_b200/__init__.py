@@ -23,7 +23,7 @@ SEL_OK, SEL_EINVAL, SEL_ENOMEM, SEL_ECUDA, SEL_ENONFINITE, SEL_EDEGENERATE, SEL_
 EB_ABS, EB_REL = 0, 1
 
 # every entry point declared in include/sel.h
-EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_batch",
+EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_multi", "sel_estimate_batch",
            "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_choose_eb",
            "sel_debug_copy", "sel_batch_layout", "sel_kernel_times",
            "sel_processed_blocks", "sel_processed_values", "sel_workspace_bytes",
@@ -73,6 +73,8 @@ def lib():
         L.sel_set_option.restype = C.c_int
         L.sel_estimate.argtypes = [P, P, P, C.POINTER(Result)]
         L.sel_estimate.restype = C.c_int
+        L.sel_estimate_multi.argtypes = [P, P, C.c_int, P, P, P]
+        L.sel_estimate_multi.restype = C.c_int
         L.sel_estimate_batch.argtypes = [P, P, C.c_int, P, P]
         L.sel_estimate_batch.restype = C.c_int
         L.sel_estimate_batch_async.argtypes = [P, P, C.c_int, P, P]
@@ -222,6 +224,16 @@ class Plan:
         _check(lib().sel_estimate(self._h, C.c_void_p(_device_ptr(field, self.shape, self.device)), _stream_ptr(stream),
                                   C.byref(r)))
         return r.to_dict()
+
+    def estimate_multi(self, field, ebs, stream=None) -> list[dict]:
+        """N1: the estimates at every error bound in `ebs` (1..8, the plan's mode) from one
+        read of `field` (sel_estimate_multi); one result dict per eb."""
+        k = len(ebs)
+        arr = (C.c_double * k)(*[float(e) for e in ebs])
+        out = (Result * k)()
+        _check(lib().sel_estimate_multi(self._h, C.c_void_p(_device_ptr(field, self.shape, self.device)), k,
+                                        arr, _stream_ptr(stream), out))
+        return [o.to_dict() for o in out]
 
     def estimate_batch(self, fields, stream=None) -> list[dict]:
         n = len(fields)

@@ -104,6 +104,13 @@ struct sel_plan_st {
   double ms[3] = {0, 0, 0};
   uint64_t tcount[3] = {0, 0, 0};
 
+  // N1 multi-eb workspace (allocated on first use): per eb a Workspace view
+  void *multi_mem = nullptr;
+  Workspace mws[kMultiMaxEb]{};
+  Params *mprm = nullptr;                         // [kMultiMaxEb]
+  Partial *mpart = nullptr;                       // [kMultiMaxEb][mcap]
+  int mcap = 0;                                   // CTA partials per eb
+
   uint64_t launches = 0;
 };
 
@@ -404,6 +411,52 @@ uint64_t real_in_processed(int64_t n, int64_t s) {
   return r;
 }
 
+// N1 multi-eb workspace: per eb a 65,536-slot histogram, CTA partials and the
+// finalize state of a Workspace (k_finalize runs once per eb on its own view)
+int ensure_multi(sel_plan_t p) {
+  if (p->multi_mem) return SEL_OK;
+  const int cap = p->sm_count * 8;                // 256-thread CTAs: occupancy <= 8
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+  const size_t o_prm = take(sizeof(Params) * kMultiMaxEb);
+  const size_t o_part = take(sizeof(Partial) * (size_t)cap * kMultiMaxEb);
+  const size_t o_h = take((size_t)kNSlots * 8 * kMultiMaxEb);   // contiguous: k_multi indexes e * kNSlots
+  size_t o_tc[kMultiMaxEb], o_fp[kMultiMaxEb], o_fe[kMultiMaxEb], o_fb[kMultiMaxEb], o_fo[kMultiMaxEb],
+      o_tk[kMultiMaxEb];
+  for (int e = 0; e < kMultiMaxEb; ++e) {
+    o_tc[e] = take(4);
+    o_fp[e] = take((size_t)kFinCTAs * 8);
+    o_fe[e] = take((size_t)kFinCTAs * 8);
+    o_fb[e] = take((size_t)kFinCTAs * 8);
+    o_fo[e] = take(16);
+    o_tk[e] = take(8);
+  }
+  if (cudaMalloc(&p->multi_mem, off) != cudaSuccess) {
+    cudaGetLastError();
+    p->multi_mem = nullptr;
+    return SEL_ENOMEM;
+  }
+  if (cudaMemset(p->multi_mem, 0, off) != cudaSuccess) return cuda_fail(cudaGetLastError(), "multi workspace");
+  char *b = (char *)p->multi_mem;
+  p->mprm = (Params *)(b + o_prm);
+  p->mpart = (Partial *)(b + o_part);
+  p->mcap = cap;
+  for (int e = 0; e < kMultiMaxEb; ++e) {
+    Workspace &w = p->mws[e];
+    w = p->ws;
+    w.hist = (unsigned long long *)(b + o_h) + (size_t)e * kNSlots;
+    w.params = p->mprm + e;
+    w.task_part = p->mpart + (size_t)e * cap;
+    w.task_ctr = (unsigned int *)(b + o_tc[e]);
+    w.fin_part = (double *)(b + o_fp[e]);
+    w.fin_err = (double *)(b + o_fe[e]);
+    w.fin_bits = (unsigned long long *)(b + o_fb[e]);
+    w.fin_ovf = (unsigned long long *)(b + o_fo[e]);
+    w.tickets = (unsigned int *)(b + o_tk[e]);
+  }
+  return SEL_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -604,6 +657,47 @@ int sel_estimate(sel_plan_t p, const float *d_field, void *stream, sel_result *o
   return SEL_OK;
 }
 
+int sel_estimate_multi(sel_plan_t p, const float *d_field, int k, const double *ebs, void *stream,
+                       sel_result *out) {
+  if (!p || !d_field || !ebs || !out || k < 1 || k > kMultiMaxEb || p->timing || p->debug) return SEL_EINVAL;
+  for (int e = 0; e < k; ++e) {
+    if (!std::isfinite(ebs[e]) || !(ebs[e] > 0.0)) return SEL_EINVAL;
+    if (p->mode == SEL_EB_ABS && !std::isfinite((float)(1.0 / (2.0 * ebs[e])))) return SEL_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_results(p, k);
+  if (rc) return rc;
+  if ((rc = ensure_multi(p))) return rc;
+  Geo g = p->geo;
+  g.vec = (g.n[2] % 4 == 0) && (((uintptr_t)d_field & 15u) == 0);
+  int ctas = 0;
+  if ((rc = multi_ctas(g, k, p->sm_count, &ctas))) return cuda_fail(cudaGetLastError(), "multi occupancy");
+  if (ctas > p->mcap) ctas = p->mcap;
+  // value range once (K1 writes vmin / vmax / non-finite into the plan's params slot)
+  const Workspace w0 = field_ws(p, 0);
+  if ((rc = launch_minmax(d_field, g.N, p->mm_ctas, w0, p->mode, p->eb, st)))
+    return cuda_fail(cudaGetLastError(), "k_minmax launch");
+  if ((rc = launch_multi(d_field, g, ctas, k, ebs, p->mode, w0.params, p->mprm, p->mws[0].hist, p->mpart, st)))
+    return rc == SEL_ECUDA ? cuda_fail(cudaGetLastError(), "k_multi launch") : rc;
+  // the per-eb part arrays are [e][ctas] inside [e][mcap] slots: k_multi writes
+  // part[e * ctas + cta] -- give every finalize its own view
+  for (int e = 0; e < k; ++e) {
+    Workspace w = p->mws[e];
+    w.task_part = p->mpart + (size_t)e * ctas;
+    FinalizeArgs fa;
+    fa.mode = p->mode;
+    fa.eb = ebs[e];
+    fa.sz_offset = p->sz_offset;
+    fa.n_sz = p->n_sz;
+    fa.n_values = p->n_values;
+    fa.n_blocks = (uint64_t)p->geo.n_pb;
+    fa.ntasks = ctas;
+    if ((rc = launch_finalize(w, fa, p->d_res + e, nullptr, st))) return cuda_fail(cudaGetLastError(), "k_finalize launch");
+  }
+  p->launches += 2 + k;
+  return finish(p, st, k, out);
+}
+
 int sel_estimate_batch(sel_plan_t p, const float *const *d_fields, int n, void *stream,
                        sel_result *out) {
   if (!p || !d_fields || !out || n < 0) return SEL_EINVAL;
@@ -792,6 +886,7 @@ void sel_plan_destroy(sel_plan_t p) {
   if (!p) return;
   if (p->copy_stream) cudaStreamSynchronize(p->copy_stream);
   if (p->ws_mem) cudaFree(p->ws_mem);
+  if (p->multi_mem) cudaFree(p->multi_mem);
   if (p->d_res) cudaFree(p->d_res);
   if (p->h_res) cudaFreeHost(p->h_res);
   if (p->dbg_mem) cudaFree(p->dbg_mem);

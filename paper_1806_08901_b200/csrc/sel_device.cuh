@@ -167,29 +167,19 @@ __device__ __forceinline__ double zfp_err_double(const int (&cf)[Tab<D>::SIZE], 
   return __dmul_rn(E, pow2d(2 * (emax - 30)));
 }
 
-// One 4^d block: v (natural order, edge-replicated) -> EC bits and gain-weighted error.
-// The sequency-ordered negabinary words are formed on the fly in ONE descending pass that
-// does both the bit count and the error classes, so a lifted coefficient dies as soon as
-// it is consumed (register pressure: the 3D block is 64 words).
-template <int D, bool DBG>
-__device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int minexp,
-                                          uint32_t &bits, double &E, int &emax,
-                                          int (&cf)[Tab<D>::SIZE], uint32_t (&u)[Tab<D>::SIZE]) {
+// ZFP stage 1 (R9, R8): block exponent, block floating point, decorrelating lift.
+// Returns false for an all-zero block (emax = -127; no transform, cf untouched).
+template <int D>
+__device__ __forceinline__ bool zfp_transform(const float (&v)[Tab<D>::SIZE], int &emax,
+                                              int (&cf)[Tab<D>::SIZE]) {
   constexpr int SZ = Tab<D>::SIZE;
-  constexpr int NC = Tab<D>::NCLS;
   // exponent (R9): max |x| as float; exponent field - 126 (subnormal max -> -126)
   float m = 0.0f;
 #pragma unroll
   for (int n = 0; n < SZ; ++n) m = fmaxf(m, fabsf(v[n]));
   if (m == 0.0f) {
     emax = -127;
-    bits = 1u;
-    E = 0.0;
-    if constexpr (DBG) {
-#pragma unroll
-      for (int n = 0; n < SZ; ++n) { cf[n] = 0; u[n] = 0u; }
-    }
-    return;
+    return false;
   }
   emax = (int)(__float_as_uint(m) >> 23) - 126;
   // block floating point: i = trunc(x 2^(30-emax)), exact (R9)
@@ -218,6 +208,21 @@ __device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int mi
 #pragma unroll
     for (int l = 0; l < 16; ++l) fwd_lift(cf[l], cf[l + 16], cf[l + 32], cf[l + 48]);
   }
+  return true;
+}
+
+// ZFP stage 2 (R10-R14) for one tolerance exponent minexp: fixed-accuracy cut, exact EC
+// bit count and gain-weighted truncation error of a transformed (non-empty) block.  The
+// sequency-ordered negabinary words are formed on the fly in ONE descending pass that
+// does both the bit count and the error classes, so a lifted coefficient dies as soon as
+// it is consumed (register pressure: the 3D block is 64 words).  Only this stage depends
+// on the error bound (through the integer minexp): the multi-eb path runs it per eb on
+// one transform.
+template <int D, bool DBG>
+__device__ __forceinline__ void zfp_cost(const int (&cf)[Tab<D>::SIZE], int emax, int minexp,
+                                         uint32_t &bits, double &E, uint32_t (&u)[Tab<D>::SIZE]) {
+  constexpr int SZ = Tab<D>::SIZE;
+  constexpr int NC = Tab<D>::NCLS;
   // fixed-accuracy cut (R12)
   int prec = emax - minexp + 2 * (D + 1);
   prec = prec < 0 ? 0 : (prec > 32 ? 32 : prec);
@@ -283,6 +288,24 @@ __device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int mi
     s = __dadd_rn(s, __dmul_rn(w, (double)acc[c]));
   });
   E = __dmul_rn(s, pow2d(2 * (emax - 30)));
+}
+
+// One 4^d block: v (natural order, edge-replicated) -> EC bits and gain-weighted error.
+template <int D, bool DBG>
+__device__ __forceinline__ void zfp_block(const float (&v)[Tab<D>::SIZE], int minexp,
+                                          uint32_t &bits, double &E, int &emax,
+                                          int (&cf)[Tab<D>::SIZE], uint32_t (&u)[Tab<D>::SIZE]) {
+  constexpr int SZ = Tab<D>::SIZE;
+  if (!zfp_transform<D>(v, emax, cf)) {
+    bits = 1u;
+    E = 0.0;
+    if constexpr (DBG) {
+#pragma unroll
+      for (int n = 0; n < SZ; ++n) { cf[n] = 0; u[n] = 0u; }
+    }
+    return;
+  }
+  zfp_cost<D, DBG>(cf, emax, minexp, bits, E, u);
 }
 
 

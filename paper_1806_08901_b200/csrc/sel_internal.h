@@ -165,5 +165,10 @@ int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Worksp
 int launch_finalize(const Workspace &ws, const FinalizeArgs &fa, sel_result *d_out,
                     unsigned long long *dbg_hist, cudaStream_t st);
 int minmax_ctas(int64_t N, int sm_count);
+// N1 multi-eb pass (sel_multi.cu)
+constexpr int kMultiMaxEb = 8;
+int multi_ctas(const Geo &g, int k, int sm_count, int *ctas);
+int launch_multi(const float *x, const Geo &g, int ctas, int k, const double *ebs, int mode,
+                 const Params *base, Params *prm, unsigned long long *hist, Partial *part, cudaStream_t st);
 
 }  // namespace sel

@@ -33,6 +33,25 @@ def run(fields, eb, stride, label):
     p.close()
 
 
+def run_multi(fields, ebs, label):
+    """N1: every eb of the sweep from one read per field (sel_estimate_multi)."""
+    shape = tuple(fields[0].shape)
+    p = sel.Plan(shape, ebs[0], "rel")
+    p.estimate_multi(fields[0], ebs)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for f in fields:
+        p.estimate_multi(f, ebs)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    gbs = len(fields) * fields[0].numel() * 4 / ms / 1e6
+    print(f"| {label} (N1: {len(ebs)} ebs, one read) | {len(fields)} | {','.join(f'{e:g}' for e in ebs)} | all | "
+          f"{ms / len(fields) * 1e3:.1f} | {gbs:.0f} (x{len(ebs)} = {gbs * len(ebs):.0f}) | {100 * gbs / PEAK:.1f} | - |",
+          flush=True)
+    p.close()
+
+
 SEL = set((sys.argv[1] if len(sys.argv) > 1 else "c1,c2,c3,c4,c5").split(","))
 print(f"| workload | fields | eb_rel | stride | us / field | GB/s | % of HBM ({PEAK:g} GB/s) | SZ / ZFP chosen |")
 print("|---|---:|---:|---|---:|---:|---:|---|")
@@ -49,6 +68,7 @@ if "c3" in SEL:
   f3 = [torch.from_numpy(synth.make_field(3, i)).cuda() for i in range(13)]
   for eb in (1e-3, 1e-4, 1e-5):
     run(f3, eb, None, "C3 100x500x500")
+  run_multi(f3, [1e-3, 1e-4, 1e-5], "C3 100x500x500")
   del f3
 if "c4" in SEL:
   f4 = [torch.from_numpy(synth.make_field(4, i)).cuda() for i in range(6)]
@@ -61,5 +81,6 @@ for mix in ((0, 1, 2) if "c5" in SEL else ()):
     x = torch.from_numpy(synth.make_field(5, mix)).cuda()
     for eb in (1e-2, 1e-4, 1e-6):
         run([x], eb, None, f"C5 1024^3 w={(0, 0.5, 1)[mix]}")
+    run_multi([x], [1e-2, 1e-3, 1e-4, 1e-5, 1e-6, 1e-7], f"C5 1024^3 w={(0, 0.5, 1)[mix]}")
     del x
     torch.cuda.empty_cache()

@@ -580,3 +580,75 @@ def test_full_config5_fields(sel, orc, mix):
         (g, o), = check_batch_exact(sel, orc, [x], eb, tag=f"C5full{mix}/{eb}")
         if mix == 2 and eb <= 1e-6:
             assert g["sz_overflow_frac"] > 0.5
+
+
+# ---------------------------------------------------------------- N1: multi-eb in one read
+@pytest.mark.parametrize("case", ["c3", "c5", "c2", "c2s", "c4s", "odd1d", "odd3d", "abs"])
+def test_multi_eb_vs_oracle(sel, orc, case):
+    """sel_estimate_multi (one read, k ebs) equals the oracle's single-eb estimate at every
+    eb: exact integer keys (histogram total / overflow, ZFP bits, minexp, choices), the
+    rest within 1e-6."""
+    import synth
+    mode, stride = "rel", None
+    if case == "c3":
+        x, ebs = synth.c3_field(5, shape=(37, 45, 70)), [1e-3, 1e-4, 1e-5]
+    elif case == "c5":
+        x, ebs = synth.c5_field(2, shape=(32, 48, 64)), [1e-2, 1e-3, 1e-4, 1e-5, 1e-6, 1e-7]
+    elif case == "c2":
+        x, ebs = synth.c2_field(3, shape=(203, 517)), [1e-2, 1e-4, 1e-6]
+    elif case == "c2s":
+        x, ebs, stride = synth.c2_field(0, shape=(120, 400)), [1e-3, 1e-4], (1, 10)
+    elif case == "c4s":
+        x, ebs, stride = synth.c4_field(0, shape=(64, 64, 64)), [1e-2, 1e-3, 1e-4, 1e-5], (4, 4, 4)
+    elif case == "odd1d":
+        rng = np.random.default_rng(11)
+        x, ebs = np.cumsum(rng.standard_normal(100003)).astype(np.float32), [1e-2, 1e-3, 1e-4, 1e-5, 1e-6, 1e-7, 1e-3, 3e-4]
+    elif case == "odd3d":
+        rng = np.random.default_rng(12)
+        x, ebs = np.cumsum(rng.standard_normal((9, 14, 21)), axis=2).astype(np.float32), [1e-2, 1e-5]
+    else:
+        x, ebs, mode = synth.c1_field(), [0.5, 0.01, 1e-4], "abs"
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    with sel.Plan(x.shape, ebs[0], mode, stride) as p:
+        l0 = p.launch_count
+        out = p.estimate_multi(t, ebs)
+        assert p.launch_count - l0 == 2 + len(ebs)        # K1, one fused pass, k finalizes
+        again = p.estimate_multi(t, ebs)
+    assert out == again                                    # deterministic, state re-zeroed
+    for e, r in zip(ebs, out):
+        o = orc.estimate(x, e, mode=mode, stride=stride)
+        compare_scalars(r, o, f"multi/{case}/{e}")
+        assert sel.choose(r) == r["choice"]
+
+
+def test_multi_eb_errors(sel):
+    t = torch.ones(8, 8, device="cuda")
+    with sel.Plan((8, 8), 1e-3) as p:
+        with pytest.raises(sel.SelError):
+            p.estimate_multi(t, [])
+        with pytest.raises(sel.SelError):
+            p.estimate_multi(t, [1e-3] * 9)
+        with pytest.raises(sel.SelError):
+            p.estimate_multi(t, [1e-3, -1.0])
+        out = p.estimate_multi(t, [1e-3, 1e-4])            # constant field, relative bound
+    assert all(r["status"] == sel.SEL_EDEGENERATE for r in out)
+    bad = torch.arange(64, dtype=torch.float32, device="cuda").view(8, 8).clone()
+    bad[2, 2] = float("inf")
+    with sel.Plan((8, 8), 1e-3) as p:
+        out = p.estimate_multi(bad, [1e-3, 1e-4])
+    assert all(r["status"] == sel.SEL_ENONFINITE for r in out)
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_multi_eb_full_size(sel, orc, cfg):
+    """Full-size N1 runs: C3 field 5 at its 3 ebs, C5 (mix 1) at its 6 ebs, from one read
+    each, against the (threaded) oracle."""
+    import synth
+    x = synth.make_field(cfg, 5 if cfg == 3 else 1)
+    ebs = synth.CONFIGS[cfg]["eb_rel"]
+    t = torch.from_numpy(x).cuda()
+    with sel.Plan(x.shape, ebs[0], "rel") as p:
+        out = p.estimate_multi(t, ebs)
+    for e, r in zip(ebs, out):
+        o = orc.estimate(x, e, mode="rel", threads=0)
+        compare_scalars(r, o, f"multi-full/C{cfg}/{e}")
