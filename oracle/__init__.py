@@ -73,6 +73,21 @@ class Result(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
 
 
+class PaperResult(C.Structure):
+    """Mirror of orc_paper_result (orc.h): the paper-literal estimator, SURVEY 8(f) N2."""
+    _fields_ = [
+        ("zfp_nsb_bits", C.c_double), ("zfp_mse_sp", C.c_double), ("zfp_psnr_sp", C.c_double),
+        ("sz_delta", C.c_double), ("sz_bits", C.c_double), ("sz_entropy", C.c_double),
+        ("sz_overflow_frac", C.c_double), ("value_range", C.c_double), ("eb_abs", C.c_double),
+        ("nsb2_total", C.c_uint64), ("n_samples", C.c_uint64), ("n_values", C.c_uint64),
+        ("hist_total", C.c_uint64), ("hist_ovf", C.c_uint64), ("r_star", C.c_float),
+        ("choice", C.c_int32), ("matched", C.c_int32), ("status", C.c_int32),
+    ]
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class Debug(C.Structure):
     _fields_ = [("codes", C.c_void_p), ("hist", C.c_void_p), ("emax", C.c_void_p),
                 ("coef", C.c_void_p), ("uword", C.c_void_p), ("bits", C.c_void_p),
@@ -91,6 +106,12 @@ def lib():
             L.orc_estimate_mt.argtypes = [P, C.c_int, P, C.c_int, C.c_double, P, C.c_double, P, P,
                                           C.c_int]
             L.orc_estimate_mt.restype = C.c_int
+            L.orc_estimate_paper.argtypes = [P, C.c_int, P, C.c_int, C.c_double, P, C.c_double, P]
+            L.orc_estimate_paper.restype = C.c_int
+            L.orc_paper_positions.argtypes = [C.c_int, P]
+            L.orc_paper_positions.restype = C.c_int
+            L.orc_block_paper.argtypes = [P, C.c_int, C.c_int, C.c_int32, P, P]
+            L.orc_block_paper.restype = None
             L.orc_processed_blocks.argtypes = [C.c_int, P, P]
             L.orc_processed_blocks.restype = C.c_uint64
             L.orc_lorenzo.argtypes = [P, C.c_int, P, P]
@@ -202,6 +223,37 @@ def estimate(x: np.ndarray, eb: float, mode: str = "rel", stride=None, sz_offset
     if debug:
         out["debug"] = arrays
     return out
+
+
+def estimate_paper(x: np.ndarray, eb: float, mode: str = "rel", stride=None,
+                   sz_offset: float = 0.5) -> dict:
+    """SURVEY 8(f) N2, the paper-literal estimator (orc_estimate_paper): BR_zfp = the
+    interpolated n_sb average of 3/9/16 sampled coefficients per block,
+    PSNR_sp from the unit-weight MSE of those samples, SZ re-quantised at the
+    delta that matches PSNR_sp (Alg. 1 lines 7-9), Alg. 1 line 10's choice."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    nd, dims, st = _dims_stride(x.shape, stride)
+    res = PaperResult()
+    st_ = lib().orc_estimate_paper(_ptr(x), nd, _ptr(dims), 1 if mode == "rel" else 0, float(eb),
+                                   None if st is None else _ptr(st), float(sz_offset), C.byref(res))
+    if st_ != 0:
+        raise OracleError(st_)
+    return res.to_dict()
+
+
+def paper_positions(nd: int) -> np.ndarray:
+    pos = np.zeros(16, np.int32)
+    m = lib().orc_paper_positions(nd, _ptr(pos))
+    return pos[:m].copy()
+
+
+def block_paper(u_seq, nd: int, kmin: int, emax: int):
+    """(2 x sum of interpolated n_sb, sum of sampled squared errors) of one block."""
+    u = np.ascontiguousarray(u_seq, dtype=np.uint32)
+    n2 = C.c_uint64()
+    mn = C.c_double()
+    lib().orc_block_paper(_ptr(u), nd, int(kmin), int(emax), C.byref(n2), C.byref(mn))
+    return int(n2.value), float(mn.value)
 
 
 # ---- single steps (pin tests) ----

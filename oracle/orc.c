@@ -638,3 +638,197 @@ int orc_estimate(const float *x, int nd, const int64_t *dims, int eb_mode, doubl
                  const int32_t *stride, double sz_offset, orc_result *out, orc_debug *dbg) {
   return orc_estimate_mt(x, nd, dims, eb_mode, eb, stride, sz_offset, out, dbg, 1);
 }
+
+/* ------------------------------------------------------------------ */
+/* the paper-literal estimator                         */
+/* ------------------------------------------------------------------ */
+/* "we sample 3 data points for one 1D data block, 9 data points for one 4x4 2D data
+ * block, and 16 data points for one 3D 4x4x4 data block".  Which points the paper's
+ * figure marks is not recoverable (figure missing); reading R19: evenly spaced
+ * over the sequency order, first and last included, j_i = round(i (4^d-1) / (m-1)),
+ * rounding halves up. */
+int orc_paper_positions(int nd, int32_t *pos) {
+  const int m = nd == 1 ? 3 : (nd == 2 ? 9 : 16);
+  const int L = (int)ipow4(nd) - 1;
+  for (int i = 0; i < m; ++i) pos[i] = (2 * i * L + (m - 1)) / (2 * (m - 1));
+  return m;
+}
+
+/* number of significant bits of a coefficient at the cut kmin: the bit planes from its
+ * leading one down to kmin (n_sb = max(0, f - kmin + 1)) */
+static int nsb_of(uint32_t u, int kmin) {
+  int f = -1;
+  for (int k = 31; k >= 0; --k) if ((u >> k) & 1u) { f = k; break; }
+  return f >= kmin ? f - kmin + 1 : 0;
+}
+
+void orc_block_paper(const uint32_t *u, int nd, int kmin, int32_t emax, uint64_t *nsb2, double *mse_num) {
+  int32_t pos[16];
+  const int m = orc_paper_positions(nd, pos);
+  int64_t n[16] = {0};
+  for (int i = 0; i < m; ++i) n[i] = nsb_of(u[pos[i]], kmin);
+  /* "use these sampled data points and their n_sb to interpolate n_sb for the remaining
+   * data points": linear interpolation along the sequency order between the
+   * neighbouring samples; the block's sum of interpolated values, doubled, is an integer:
+   * sum over segment a of (len n_a + (n_{a+1} - n_a) t) / len, t = 0..len-1 */
+  int64_t two_sum = 0;
+  for (int a = 0; a + 1 < m; ++a) {
+    const int64_t len = pos[a + 1] - pos[a];
+    int64_t num = 0;                          /* sum_t (len n_a + (n_{a+1} - n_a) t) */
+    for (int64_t t = 0; t < len; ++t) num += len * n[a] + (n[a + 1] - n[a]) * t;
+    two_sum += 2 * num / len;                 /* exact: = 2 len n_a + (n_{a+1}-n_a)(len-1) */
+  }
+  two_sum += 2 * n[m - 1];                     /* the last position */
+  *nsb2 = (uint64_t)two_sum;
+  /* MSE_sp: "each sampled data point's error is calculated by multiplication of its
+   * truncated error in binary representation and its block's exponent offset value"
+   * (P:456): e = value of the dropped bit planes (< kmin) of the negabinary word,
+   * times 2^(emax - 30), squared; unit weights (the paper's reading; R14 is ours) */
+  double acc = 0.0;
+  const double scale = ldexp(1.0, 2 * (emax - 30));
+  for (int i = 0; i < m; ++i) {
+    const uint32_t uj = u[pos[i]];
+    const uint32_t low = kmin >= 32 ? 0xffffffffu : ((1u << kmin) - 1u);
+    const int64_t c = (int64_t)orc_negabinary_inv(uj);
+    const int64_t ct = (int64_t)orc_negabinary_inv(uj & ~low);    /* planes >= kmin kept */
+    const double e = (double)(c - ct);
+    acc += e * e * scale;
+  }
+  *mse_num = acc;
+}
+
+int orc_estimate_paper(const float *x, int nd, const int64_t *dims, int eb_mode, double eb,
+                       const int32_t *stride, double sz_offset, orc_paper_result *out) {
+  if (nd < 1 || nd > 3 || !x || !dims || !out) return ORC_EINVAL;
+  int64_t N = 1;
+  for (int a = 0; a < nd; ++a) { if (dims[a] < 1) return ORC_EINVAL; N *= dims[a]; }
+  int32_t s[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) { s[a] = stride ? stride[a] : 1; if (s[a] < 1) return ORC_EINVAL; }
+  if (!isfinite(eb) || !(eb > 0.0) || (eb_mode != 0 && eb_mode != 1)) return ORC_EINVAL;
+  /* Alg. 1 line 2: VR and eb */
+  float vmin = x[0], vmax = x[0];
+  for (int64_t i = 0; i < N; ++i) {
+    if (!isfinite(x[i])) return ORC_ENONFINITE;
+    if (x[i] < vmin) vmin = x[i];
+    if (x[i] > vmax) vmax = x[i];
+  }
+  const double VR = (double)vmax - (double)vmin;
+  const double eb_abs = (eb_mode == 1) ? eb * VR : eb;
+  if (eb_mode == 1 && VR == 0.0) return ORC_EDEGENERATE;
+  if (!isfinite((float)(1.0 / (2.0 * eb_abs))) || !(eb_abs > 0.0)) return ORC_EINVAL;
+  int fe; frexp(eb_abs, &fe);
+  const int32_t minexp = fe - 1;
+  const int size = (int)ipow4(nd);
+  int32_t perm[64], pos[16];
+  orc_sequency_perm(nd, perm);
+  const int m = orc_paper_positions(nd, pos);
+  int64_t nb[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) nb[a] = (dims[a] + 3) / 4;
+  const int64_t nblocks_all = nb[0] * nb[1] * nb[2];
+  /* Alg. 1 lines 3-6: blockwise sample, then the ZFP estimate of each block
+   * from its sampled coefficients */
+  uint64_t nsb2_total = 0, n_samples = 0, n_values = 0;
+  double mse_sum = 0.0;
+  for (int64_t lb = 0; lb < nblocks_all; ++lb) {
+    int64_t b[3], r = lb;
+    for (int a = nd - 1; a >= 0; --a) { b[a] = r % nb[a]; r /= nb[a]; }
+    int processed = 1;
+    for (int a = 0; a < nd; ++a) if (b[a] % s[a] != 0) processed = 0;
+    if (!processed) continue;
+    float blk[64];
+    for (int n = 0; n < size; ++n) {
+      int64_t idx[3], cl[3];
+      int inside = 1, rr = n;
+      for (int a = nd - 1; a >= 0; --a) {
+        int o = rr % 4; rr /= 4;
+        idx[a] = 4 * b[a] + o;
+        if (idx[a] >= dims[a]) inside = 0;
+        cl[a] = idx[a] < dims[a] ? idx[a] : dims[a] - 1;     /* edge replication (R17) */
+      }
+      int64_t lin = 0;
+      for (int a = 0; a < nd; ++a) lin = lin * dims[a] + cl[a];
+      blk[n] = x[lin];
+      n_values += inside ? 1 : 0;
+    }
+    uint32_t u[64];
+    int32_t emax = orc_block_emax(blk, size);
+    int kmin = 32;
+    if (emax == -127) {
+      for (int j = 0; j < size; ++j) u[j] = 0;
+      emax = -126;                                /* (no error, no significant bit) */
+    } else {
+      int32_t coef[64];
+      orc_block_bfp(blk, size, emax, coef);
+      orc_fwd_xform(coef, nd);
+      for (int j = 0; j < size; ++j) u[j] = orc_negabinary(coef[perm[j]]);
+      kmin = 32 - orc_precision(emax, minexp, nd);
+    }
+    uint64_t nsb2;
+    double mn;
+    orc_block_paper(u, nd, kmin, emax, &nsb2, &mn);
+    nsb2_total += nsb2;
+    mse_sum += mn;
+    n_samples += (uint64_t)m;
+  }
+  memset(out, 0, sizeof(*out));
+  out->value_range = VR;
+  out->eb_abs = eb_abs;
+  out->nsb2_total = nsb2_total;
+  out->n_samples = n_samples;
+  out->n_values = n_values;
+  out->zfp_nsb_bits = (double)nsb2_total / 2.0 / (double)n_values;
+  out->zfp_mse_sp = mse_sum / (double)n_samples;
+  /* PSNR_sp = -10 log10 MSE_sp + 20 log10 VR */
+  out->zfp_psnr_sp = out->zfp_mse_sp > 0.0 ? 20.0 * log10(VR) - 10.0 * log10(out->zfp_mse_sp) : INFINITY;
+  /* Alg. 1 line 7: delta with PSNR_sz = PSNR_sp in Eq. psnr-pdf-linear:
+   * delta = VR sqrt(12) 10^(-PSNR_sp/20) = sqrt(12 MSE_sp).  MSE_sp == 0 (or VR == 0):
+   * no PSNR to match -- SZ at the user's bound (delta = 2 eb_abs), matched = 0 (R16 ii) */
+  double delta = out->zfp_mse_sp > 0.0 && VR > 0.0 ? sqrt(12.0 * out->zfp_mse_sp) : 2.0 * eb_abs;
+  float rs = (float)(1.0 / delta);
+  out->matched = out->zfp_mse_sp > 0.0 && VR > 0.0 && isfinite(rs) ? 1 : 0;
+  if (!out->matched) { delta = 2.0 * eb_abs; rs = (float)(1.0 / delta); }
+  out->sz_delta = delta;
+  out->r_star = rs;
+  /* Alg. 1 lines 8-9: the residual density of the sampled blocks at bin width delta
+   * (linear quantisation R5 with r = 1/delta), Eq. bitrate-sz = its entropy,
+   * + offset + 32 p_ovf (R6) */
+  uint64_t *hist = (uint64_t *)calloc(ORC_NSLOTS, sizeof(uint64_t));
+  if (!hist) return ORC_EINVAL;
+  uint64_t n_sz = 0;
+  for (int64_t lb = 0; lb < nblocks_all; ++lb) {
+    int64_t b[3], r = lb;
+    for (int a = nd - 1; a >= 0; --a) { b[a] = r % nb[a]; r /= nb[a]; }
+    int processed = 1;
+    for (int a = 0; a < nd; ++a) if (b[a] % s[a] != 0) processed = 0;
+    if (!processed) continue;
+    for (int n = 0; n < size; ++n) {
+      int64_t idx[3];
+      int inside = 1, origin = 1, rr = n;
+      for (int a = nd - 1; a >= 0; --a) {
+        int o = rr % 4; rr /= 4;
+        idx[a] = 4 * b[a] + o;
+        if (idx[a] >= dims[a]) inside = 0;
+        if (idx[a] != 0) origin = 0;
+      }
+      if (!inside || origin) continue;
+      hist[orc_quantize(orc_lorenzo(x, nd, dims, idx), rs)] += 1;
+      ++n_sz;
+    }
+  }
+  int rc = ORC_OK;
+  if (n_sz == 0) rc = ORC_EDEGENERATE;
+  else {
+    out->sz_entropy = orc_entropy_counts(hist, ORC_NSLOTS);
+    out->sz_overflow_frac = (double)hist[ORC_OVF_SLOT] / (double)n_sz;
+    out->sz_bits = out->sz_entropy + sz_offset + 32.0 * out->sz_overflow_frac;
+    uint64_t tot = 0;
+    for (int k = 0; k < ORC_NSLOTS; ++k) tot += hist[k];
+    out->hist_total = tot;
+    out->hist_ovf = hist[ORC_OVF_SLOT];
+    /* Alg. 1 line 10: SZ iff BR_sz < BR_zfp, else ZFP */
+    out->choice = out->sz_bits < out->zfp_nsb_bits ? 0 : 1;
+  }
+  out->status = rc;
+  free(hist);
+  return rc;
+}

@@ -73,6 +73,41 @@ int orc_estimate_mt(const float *x, int ndims, const int64_t *dims, int eb_mode,
                     orc_result *out, orc_debug *dbg, int nthreads);
 uint64_t orc_processed_blocks(int ndims, const int64_t *dims, const int32_t *stride);
 
+/* ---- the paper-literal estimator (Alg. 1 lines 3-10 as printed) ----
+ * ZFP: n_sb of 3 / 9 / 16 sampled coefficients per 1D / 2D / 3D block, linear
+ * interpolation of n_sb over the block's sequency order, average = BR_zfp;
+ * MSE_sp = mean over the sampled coefficients of (truncated error x block exponent
+ * offset)^2, unit weights.  SZ: delta from PSNR_sp (Alg. 1 line 7, Eq.
+ * psnr-pdf-linear P:403), the Lorenzo residuals of the processed blocks re-quantised at
+ * bin width delta, BR_sz = entropy (Eq. bitrate-sz) + offset + 32 p_ovf. */
+typedef struct {
+  double zfp_nsb_bits;    /* n_sb average: nsb2_total / 2 / n_values                       */
+  double zfp_mse_sp;      /* sum of sampled squared errors / n_samples                      */
+  double zfp_psnr_sp;     /* 20 log10 VR - 10 log10 MSE_sp; +INF if MSE_sp == 0             */
+  double sz_delta;        /* sqrt(12 MSE_sp) (= VR sqrt(12) 10^(-PSNR_sp/20)); 2 eb_abs if   */
+                          /* MSE_sp == 0 (matched = 0)                                      */
+  double sz_bits;         /* H(delta) + offset + 32 p_ovf                                    */
+  double sz_entropy;
+  double sz_overflow_frac;
+  double value_range, eb_abs;
+  uint64_t nsb2_total;    /* 2 x sum of the interpolated n_sb (an exact integer)            */
+  uint64_t n_samples;     /* sampled coefficients = m x processed blocks                    */
+  uint64_t n_values;      /* real values in processed blocks                                */
+  uint64_t hist_total, hist_ovf;
+  float r_star;           /* float(1 / delta), the quantiser scale of the SZ re-quantisation */
+  int32_t choice;         /* 0 = SZ iff sz_bits < zfp_nsb_bits (Alg. 1 line 10)              */
+  int32_t matched;
+  int32_t status;
+} orc_paper_result;
+int orc_estimate_paper(const float *x, int ndims, const int64_t *dims, int eb_mode, double eb,
+                       const int32_t *stride, double sz_offset, orc_paper_result *out);
+/* the sampled sequency positions j_i = round(i (4^d - 1) / (m - 1)), i < m */
+int orc_paper_positions(int ndims, int32_t *pos);
+/* one block: 2 x sum of the linearly interpolated n_sb and the sum of the sampled squared
+ * errors (value units), from the sequency-ordered negabinary words */
+void orc_block_paper(const uint32_t *u_seq, int ndims, int kmin, int32_t emax, uint64_t *nsb2,
+                     double *mse_num);
+
 /* ---- single steps, exported for the pin tests ---- */
 float orc_lorenzo(const float *x, int ndims, const int64_t *dims, const int64_t *idx);
 int32_t orc_quantize(float d, float r_f);

@@ -670,3 +670,102 @@ def test_full_estimate_sanity_c1(orc):
     assert r["zfp_psnr"] > r["sz_psnr"]
     assert r["matched"] == 1
     assert r["sz_eb_matched"] < r["eb_abs"]
+
+
+# ------------------------------------------------------ N2: paper-literal estimator
+@pytest.mark.parametrize("nd,m", [(1, 3), (2, 9), (3, 16)])
+def test_paper_sample_positions(orc, nd, m):
+    """3 / 9 / 16 sampled points per 1D / 2D / 3D block; reading R19: evenly spaced
+    over the sequency order, first and last coefficient included."""
+    pos = orc.paper_positions(nd)
+    L = 4 ** nd - 1
+    assert len(pos) == m and pos[0] == 0 and pos[-1] == L
+    assert np.all(np.diff(pos) > 0)
+    # evenly spaced: every position within half a step of i L / (m - 1)
+    assert np.all(np.abs(pos - np.arange(m) * L / (m - 1)) <= 0.5)
+
+
+def _nsb(u, kmin):
+    u = int(u)
+    return max(0, u.bit_length() - 1 - kmin + 1) if u else 0
+
+
+@pytest.mark.parametrize("nd", [1, 2, 3])
+def test_paper_block_interpolation_and_error(orc, nd):
+    """orc_block_paper against the definitions written independently: n_sb at the samples
+    (leading one down to the cut, A13), numpy.interp of n_sb over every sequency position
+    (P:448-449), and the sampled error = value of the dropped negabinary planes
+    ((u & low) ^ M) - M (a different formula from the oracle's c - c~) times the block
+    exponent offset, squared."""
+    rng = np.random.default_rng(40 + nd)
+    size = 4 ** nd
+    pos = orc.paper_positions(nd)
+    for _ in range(200):
+        # a staircase-like sequency vector: magnitudes decaying with j, random signs
+        mag = (2.0 ** (rng.uniform(0, 29, size) * np.exp(-np.arange(size) / rng.uniform(2, 30))))
+        c = (mag * rng.choice([-1, 1], size)).astype(np.int64).clip(-(1 << 30) + 1, (1 << 30) - 1)
+        u = np.array([orc.negabinary(int(v)) for v in c], np.uint32)
+        kmin = int(rng.integers(0, 33))
+        emax = int(rng.integers(-20, 20))
+        n2, mse = orc.block_paper(u, nd, kmin, emax)
+        ns = np.array([_nsb(u[p], kmin) for p in pos], np.float64)
+        interp = np.interp(np.arange(size), pos, ns)
+        assert abs(n2 - 2.0 * interp.sum()) < 1e-6, (n2, 2 * interp.sum())
+        low = (1 << kmin) - 1
+        M = 0xAAAAAAAA & low
+        ref = 0.0
+        for p in pos:
+            e = ((int(u[p]) & low) ^ M) - M
+            ref += float(e) * float(e) * 2.0 ** (2 * (emax - 30))
+        assert math.isclose(mse, ref, rel_tol=1e-12, abs_tol=0.0) or (mse == 0.0 and ref == 0.0)
+    # constant n_sb over the block -> 2 * size * n exactly
+    u = np.full(size, 0b101 << 10, np.uint32)
+    n2, _ = orc.block_paper(u, nd, 8, 0)
+    assert n2 == 2 * size * (12 - 8 + 1)
+
+
+def test_paper_estimate_properties(orc):
+    """Alg. 1 lines 3-10 as printed: delta from PSNR_sp by Eq. psnr-pdf-linear,
+    BR_zfp = average interpolated n_sb, choice by line 10."""
+    import synth
+    x = synth.c1_field()
+    r = orc.estimate_paper(x, 1e-4)
+    assert r["status"] == 0 and r["matched"] == 1
+    assert r["n_samples"] == 9 * 4096 and r["n_values"] == 65536
+    assert r["zfp_nsb_bits"] == r["nsb2_total"] / 2 / r["n_values"]
+    # delta = VR sqrt(12) 10^(-PSNR_sp / 20)   (Eq. psnr-pdf-linear with PSNR_sz = PSNR_sp)
+    d = r["value_range"] * math.sqrt(12.0) * 10.0 ** (-r["zfp_psnr_sp"] / 20.0)
+    assert math.isclose(r["sz_delta"], d, rel_tol=1e-12)
+    assert math.isclose(r["zfp_psnr_sp"], 20 * math.log10(r["value_range"]) - 10 * math.log10(r["zfp_mse_sp"]),
+                        rel_tol=1e-14)
+    assert r["hist_total"] == 65535
+    assert r["choice"] == (0 if r["sz_bits"] < r["zfp_nsb_bits"] else 1)
+    # the literal reading's unit weights make PSNR_sp optimistic vs the gain-weighted PSNR
+    # (SURVEY 8(c) A14: ~4^d low MSE in 2D)
+    g = orc.estimate(x, 1e-4)
+    assert r["zfp_psnr_sp"] > g["zfp_psnr"] + 6.0
+
+
+def test_paper_unmatched_equals_regular_sz(orc):
+    """No truncation at any sample (a tiny absolute bound: p = 32, kmin = 0) -> MSE_sp = 0,
+    no PSNR to match: SZ at the user's bound, delta = 2 eb_abs (R16 ii), and then the
+    re-quantised SZ estimate IS the regular one (same bins), bit for bit."""
+    rng = np.random.default_rng(5)
+    x = (1.0 + 0.25 * rng.standard_normal((24, 40))).astype(np.float32)
+    eb = 2.0 ** -40
+    r = orc.estimate_paper(x, eb, mode="abs")
+    g = orc.estimate(x, eb, mode="abs")
+    assert r["zfp_mse_sp"] == 0.0 and math.isinf(r["zfp_psnr_sp"]) and r["matched"] == 0
+    assert r["sz_delta"] == 2 * eb
+    assert r["sz_bits"] == g["sz_bits_per_value"] and r["hist_total"] == g["hist_total"]
+
+
+def test_paper_sampled_blocks(orc):
+    """Alg. 1 line 3: with strides, only the processed blocks enter both the
+    ZFP samples and the SZ residual histogram."""
+    import synth
+    x = synth.c2_field(1, shape=(80, 160))
+    r = orc.estimate_paper(x, 1e-4, stride=(1, 10))
+    nb = orc.processed_blocks(x.shape, (1, 10))
+    assert r["n_samples"] == 9 * nb
+    assert r["hist_total"] == 16 * nb - 1          # every real point but the origin
