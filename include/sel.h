@@ -89,6 +89,31 @@ typedef struct {
   uint64_t hist_ovf;         /* count in the overflow slot 65,535, device-counted              */
 } sel_result;
 
+/* the paper's own estimator as printed (Alg. 1 lines 3-10),
+ * reported next to the exact estimate of sel_estimate (which counts every coefficient's
+ * EC bits and gain-weights the error, R13/R14). */
+typedef struct {
+  double zfp_nsb_bits;       /* BR_zfp: average n_sb, 3/9/16 sampled coefficients per block     */
+                             /* linearly interpolated over the block          */
+  double zfp_mse_sp;         /* MSE_sp: mean (dropped-plane value x 2^(emax-30))^2 of the samples */
+                             /* (unit weights)                                        */
+  double zfp_psnr_sp;        /* -10 log10 MSE_sp + 20 log10 VR; +INF if MSE_sp == 0              */
+  double sz_delta;           /* delta = VR sqrt(12) 10^(-PSNR_sp/20) (Alg.1 line 7); 2 eb_abs if  */
+                             /* matched == 0                                                     */
+  double sz_bits;            /* BR_sz: entropy of the residuals at bin width delta + 0.5 + 32 p_ovf */
+  double sz_entropy;
+  double sz_overflow_frac;
+  double value_range, eb_abs;
+  uint64_t nsb2_total;       /* 2 x sum of the interpolated n_sb (exact integer)                 */
+  uint64_t n_samples;        /* sampled coefficients (m x processed blocks)                      */
+  uint64_t n_values;         /* real values in processed blocks                                  */
+  uint64_t hist_total, hist_ovf;
+  float r_star;              /* float(1 / delta), the quantiser scale of the re-quantisation      */
+  int32_t choice;            /* Alg.1 line 10: 0 = SZ iff sz_bits < zfp_nsb_bits, else 1 = ZFP    */
+  int32_t matched;           /* 0: MSE_sp == 0 or VR == 0, compared at the user's bound           */
+  int32_t status;
+} sel_paper_result;
+
 /* Create a plan for fields of shape dims[0..ndims-1].
  *   mode, eb : SEL_EB_ABS -> eb_abs = eb; SEL_EB_REL -> eb_abs = eb * VR (Alg.1 line 2)
  *   stride   : ndims entries >= 1, block b is processed iff b_a % stride[a] == 0 for
@@ -122,6 +147,14 @@ int sel_set_option(sel_plan_t plan, const char *key, double value);
  * result to pinned host memory, synchronises `stream`, fills *out.
  * Errors: SEL_EINVAL, SEL_ENONFINITE, SEL_EDEGENERATE, SEL_ECUDA. */
 int sel_estimate(sel_plan_t plan, const float *d_field, void *stream, sel_result *out);
+
+/* N2: the paper-literal estimate of one device field with the plan's eb,
+ * mode and stride (sel_paper_result above).  Two dependent passes, as Alg. 1 prints them:
+ * the ZFP samples give PSNR_sp, whose delta fixes the SZ re-quantisation of the same
+ * processed blocks.  d_field: device, float32, C order; synchronises `stream`.
+ * Errors: SEL_EINVAL (NULL, options debug / kernel_timing set), SEL_ENONFINITE,
+ * SEL_EDEGENERATE (status also in out->status), SEL_ENOMEM, SEL_ECUDA. */
+int sel_estimate_paper(sel_plan_t plan, const float *d_field, void *stream, sel_paper_result *out);
 
 /* N1: the rate-distortion curve of one field at k error bounds from ONE read
  * (P:384-392 -- rate-distortion compared over error bounds; Alg. 1 lines 2-10 per eb,

@@ -23,11 +23,27 @@ SEL_OK, SEL_EINVAL, SEL_ENOMEM, SEL_ECUDA, SEL_ENONFINITE, SEL_EDEGENERATE, SEL_
 EB_ABS, EB_REL = 0, 1
 
 # every entry point declared in include/sel.h
-EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_multi", "sel_estimate_batch",
+EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_multi", "sel_estimate_paper",
+           "sel_estimate_batch",
            "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_choose_eb",
            "sel_debug_copy", "sel_batch_layout", "sel_kernel_times",
            "sel_processed_blocks", "sel_processed_values", "sel_workspace_bytes",
            "sel_launch_count", "sel_plan_destroy", "sel_strerror")
+
+
+class PaperResult(C.Structure):
+    """Mirror of ``sel_paper_result`` (include/sel.h)."""
+    _fields_ = [
+        ("zfp_nsb_bits", C.c_double), ("zfp_mse_sp", C.c_double), ("zfp_psnr_sp", C.c_double),
+        ("sz_delta", C.c_double), ("sz_bits", C.c_double), ("sz_entropy", C.c_double),
+        ("sz_overflow_frac", C.c_double), ("value_range", C.c_double), ("eb_abs", C.c_double),
+        ("nsb2_total", C.c_uint64), ("n_samples", C.c_uint64), ("n_values", C.c_uint64),
+        ("hist_total", C.c_uint64), ("hist_ovf", C.c_uint64), ("r_star", C.c_float),
+        ("choice", C.c_int32), ("matched", C.c_int32), ("status", C.c_int32),
+    ]
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 class SelError(RuntimeError):
@@ -73,6 +89,8 @@ def lib():
         L.sel_set_option.restype = C.c_int
         L.sel_estimate.argtypes = [P, P, P, C.POINTER(Result)]
         L.sel_estimate.restype = C.c_int
+        L.sel_estimate_paper.argtypes = [P, P, P, C.POINTER(PaperResult)]
+        L.sel_estimate_paper.restype = C.c_int
         L.sel_estimate_multi.argtypes = [P, P, C.c_int, P, P, P]
         L.sel_estimate_multi.restype = C.c_int
         L.sel_estimate_batch.argtypes = [P, P, C.c_int, P, P]
@@ -223,6 +241,14 @@ class Plan:
         r = Result()
         _check(lib().sel_estimate(self._h, C.c_void_p(_device_ptr(field, self.shape, self.device)), _stream_ptr(stream),
                                   C.byref(r)))
+        return r.to_dict()
+
+    def estimate_paper(self, field, stream=None) -> dict:
+        """N2: the paper-literal estimate (sel_estimate_paper): sampled-coefficient n_sb
+        bit-rate, unit-weight PSNR_sp, SZ re-quantised at the matching delta."""
+        r = PaperResult()
+        _check(lib().sel_estimate_paper(self._h, C.c_void_p(_device_ptr(field, self.shape, self.device)),
+                                        _stream_ptr(stream), C.byref(r)))
         return r.to_dict()
 
     def estimate_multi(self, field, ebs, stream=None) -> list[dict]:

@@ -111,6 +111,10 @@ struct sel_plan_st {
   Partial *mpart = nullptr;                       // [kMultiMaxEb][mcap]
   int mcap = 0;                                   // CTA partials per eb
 
+  // N2 paper-literal workspace (first use): CTA partials, mid scalars, params, result
+  void *paper_mem = nullptr;
+  int paper_cap = 0;
+
   uint64_t launches = 0;
 };
 
@@ -657,6 +661,63 @@ int sel_estimate(sel_plan_t p, const float *d_field, void *stream, sel_result *o
   return SEL_OK;
 }
 
+int sel_estimate_paper(sel_plan_t p, const float *d_field, void *stream, sel_paper_result *out) {
+  if (!p || !d_field || !out || p->timing || p->debug) return SEL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_results(p, 1);
+  if (rc) return rc;
+  // workspace: [CTA partials | mid | Params | sel_paper_result], allocated once per plan
+  const int cap = p->sm_count * 8;
+  const size_t pws = paper_ws_bytes(cap);
+  if (!p->paper_mem) {
+    if (cudaMalloc(&p->paper_mem, pws + 2 * sizeof(Params) + sizeof(sel_paper_result) + 512) != cudaSuccess) {
+      cudaGetLastError();
+      p->paper_mem = nullptr;
+      return SEL_ENOMEM;
+    }
+    p->paper_cap = cap;
+  }
+  char *b = (char *)p->paper_mem;
+  Params *pprm = (Params *)(b + ((pws + 255) & ~(size_t)255));
+  sel_paper_result *dres = (sel_paper_result *)(pprm + 2);
+  Geo g = p->geo;
+  g.vec = (g.n[2] % 4 == 0) && (((uintptr_t)d_field & 15u) == 0);
+  // Alg. 1 line 2: value range (params slot 0 of the plan)
+  const Workspace w0 = field_ws(p, 0);
+  if ((rc = launch_minmax(d_field, g.N, p->mm_ctas, w0, p->mode, p->eb, st)))
+    return cuda_fail(cudaGetLastError(), "k_minmax launch");
+  // lines 3-7: ZFP from the sampled coefficients -> PSNR_sp -> delta, r* = 1/delta
+  if ((rc = launch_paper_zfp(d_field, g, p->sm_count, p->paper_cap, w0.params, p->paper_mem, pprm, st)))
+    return cuda_fail(cudaGetLastError(), "k_paper_zfp launch");
+  // lines 8-9: the processed blocks' residuals at bin width delta (the fused pass with
+  // r_f = r*; only its histogram is used), entropy in the finalize
+  Workspace ws = p->wsk[0];
+  ws.params = pprm;
+  const bool tile = p->tile_ok && g.vec;
+  rc = tile ? launch_tile(d_field, g, p->tl[0], ws, nullptr, st)
+            : launch_estimate(d_field, g, p->el[g.vec][0], ws, nullptr, st);
+  if (rc) return cuda_fail(cudaGetLastError(), "paper SZ pass launch");
+  FinalizeArgs fa;
+  fa.mode = p->mode;
+  fa.eb = p->eb;
+  fa.sz_offset = p->sz_offset;
+  fa.n_sz = p->n_sz;
+  fa.n_values = p->n_values;
+  fa.n_blocks = (uint64_t)p->geo.n_pb;
+  fa.ntasks = tile ? p->tl[0].npart : p->el[g.vec][0].ntasks;
+  if ((rc = launch_finalize(ws, fa, p->d_res, nullptr, st))) return cuda_fail(cudaGetLastError(), "k_finalize launch");
+  // line 10 + the result
+  if ((rc = launch_paper_assemble(p->paper_mem, p->paper_cap, p->d_res, p->n_values, dres, st)))
+    return cuda_fail(cudaGetLastError(), "k_paper_assemble launch");
+  p->launches += 6;
+  sel_paper_result h;
+  CK(cudaMemcpyAsync(&h, dres, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h.status != SEL_OK) return h.status;
+  *out = h;
+  return SEL_OK;
+}
+
 int sel_estimate_multi(sel_plan_t p, const float *d_field, int k, const double *ebs, void *stream,
                        sel_result *out) {
   if (!p || !d_field || !ebs || !out || k < 1 || k > kMultiMaxEb || p->timing || p->debug) return SEL_EINVAL;
@@ -887,6 +948,7 @@ void sel_plan_destroy(sel_plan_t p) {
   if (p->copy_stream) cudaStreamSynchronize(p->copy_stream);
   if (p->ws_mem) cudaFree(p->ws_mem);
   if (p->multi_mem) cudaFree(p->multi_mem);
+  if (p->paper_mem) cudaFree(p->paper_mem);
   if (p->d_res) cudaFree(p->d_res);
   if (p->h_res) cudaFreeHost(p->h_res);
   if (p->dbg_mem) cudaFree(p->dbg_mem);

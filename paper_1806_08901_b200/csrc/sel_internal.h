@@ -165,6 +165,12 @@ int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Worksp
 int launch_finalize(const Workspace &ws, const FinalizeArgs &fa, sel_result *d_out,
                     unsigned long long *dbg_hist, cudaStream_t st);
 int minmax_ctas(int64_t N, int sm_count);
+// N2 paper-literal estimator (sel_paper.cu)
+size_t paper_ws_bytes(int max_ctas);
+int launch_paper_zfp(const float *x, const Geo &g, int sm_count, int max_ctas, const Params *base, void *pws,
+                     Params *pprm, cudaStream_t st);
+int launch_paper_assemble(void *pws, int max_ctas, const sel_result *sz, uint64_t n_values, sel_paper_result *out,
+                          cudaStream_t st);
 // N1 multi-eb pass (sel_multi.cu)
 constexpr int kMultiMaxEb = 8;
 int multi_ctas(const Geo &g, int k, int sm_count, int *ctas);

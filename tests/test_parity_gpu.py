@@ -652,3 +652,80 @@ def test_multi_eb_full_size(sel, orc, cfg):
     for e, r in zip(ebs, out):
         o = orc.estimate(x, e, mode="rel", threads=0)
         compare_scalars(r, o, f"multi-full/C{cfg}/{e}")
+
+
+# ---------------------------------------------------------------- N2: paper-literal estimator
+PAPER_EXACT = ("nsb2_total", "n_samples", "n_values", "hist_total", "hist_ovf", "r_star", "choice",
+               "matched", "status")
+PAPER_CLOSE = ("zfp_nsb_bits", "zfp_mse_sp", "zfp_psnr_sp", "sz_delta", "sz_bits", "sz_entropy",
+               "sz_overflow_frac", "value_range", "eb_abs")
+
+
+def compare_paper(g, o, tag=""):
+    for k in PAPER_EXACT:
+        assert g[k] == o[k], (tag, k, g[k], o[k])
+    for k in PAPER_CLOSE:
+        assert close(float(g[k]), float(o[k])), (tag, k, g[k], o[k])
+
+
+@pytest.mark.parametrize("case", ["c1", "c2r", "c2s", "c3r", "c4s", "c5", "odd1d", "odd2d", "unmatched"])
+def test_paper_estimator_vs_oracle(sel, orc, case):
+    """sel_estimate_paper (Alg. 1 lines 3-10 as printed) equals the oracle:
+    the interpolated n_sb total, sample count, histogram at delta and the choice exactly,
+    the rest within 1e-6."""
+    import synth
+    mode, stride, eb = "rel", None, 1e-4
+    if case == "c1":
+        x = synth.c1_field()
+    elif case == "c2r":
+        x = synth.c2_field(0, shape=(203, 516))
+    elif case == "c2s":
+        x, stride = synth.c2_field(3, shape=(120, 400)), (1, 10)
+    elif case == "c3r":
+        x, eb = synth.c3_field(5, shape=(37, 45, 70)), 1e-5
+    elif case == "c4s":
+        x, stride = synth.c4_field(0, shape=(64, 64, 64)), (4, 4, 4)
+    elif case == "c5":
+        x, eb = synth.c5_field(1, shape=(32, 48, 64)), 1e-6
+    elif case == "odd1d":
+        x = np.cumsum(np.random.default_rng(3).standard_normal(10007)).astype(np.float32)
+    elif case == "odd2d":
+        x = np.cumsum(np.random.default_rng(4).standard_normal((13, 27)), axis=1).astype(np.float32)
+    else:
+        rng = np.random.default_rng(5)
+        x, eb, mode = (1.0 + 0.25 * rng.standard_normal((24, 40))).astype(np.float32), 2.0 ** -40, "abs"
+    o = orc.estimate_paper(x, eb, mode=mode, stride=stride)
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    with sel.Plan(x.shape, eb, mode, stride) as p:
+        l0 = p.launch_count
+        g = p.estimate_paper(t)
+        assert p.launch_count - l0 == 6
+        g2 = p.estimate_paper(t)
+        e = p.estimate(t)                            # the exact estimate still works after it
+    assert g == g2
+    compare_paper(g, o, case)
+    compare_scalars(e, orc.estimate(x, eb, mode=mode, stride=stride), case + "/exact-after")
+    if case == "unmatched":
+        assert g["matched"] == 0 and g["sz_bits"] == e["sz_bits_per_value"]
+
+
+def test_paper_estimator_full_size(sel, orc):
+    """C4 field 0 (512^3) at 1/64 block sampling and a full C2 field, against the oracle."""
+    import synth
+    for x, stride in ((synth.c4_field(0), (4, 4, 4)), (synth.c2_field(10), None)):
+        o = orc.estimate_paper(x, 1e-4, stride=stride)
+        with sel.Plan(x.shape, 1e-4, "rel", stride) as p:
+            g = p.estimate_paper(torch.from_numpy(x).cuda())
+        compare_paper(g, o, f"full{x.shape}")
+
+
+def test_paper_estimator_errors(sel):
+    with sel.Plan((8, 8), 1e-3) as p:
+        with pytest.raises(sel.SelError) as e:
+            p.estimate_paper(torch.ones(8, 8, device="cuda"))
+        assert e.value.status == sel.SEL_EDEGENERATE
+        bad = torch.arange(64, dtype=torch.float32, device="cuda").view(8, 8).clone()
+        bad[1, 1] = float("nan")
+        with pytest.raises(sel.SelError) as e:
+            p.estimate_paper(bad)
+        assert e.value.status == sel.SEL_ENONFINITE
