@@ -112,6 +112,11 @@ def lib():
             L.orc_paper_positions.restype = C.c_int
             L.orc_block_paper.argtypes = [P, C.c_int, C.c_int, C.c_int32, P, P]
             L.orc_block_paper.restype = None
+            L.orc_zfp_stream.argtypes = [P, C.c_int, P, C.c_int, C.c_double, P, P, C.c_uint64, P]
+            L.orc_zfp_stream.restype = C.c_int
+            L.orc_zfp_stream_decode.argtypes = [P, C.c_uint64, C.c_int, P, C.c_int, C.c_double, C.c_double,
+                                                P, P]
+            L.orc_zfp_stream_decode.restype = C.c_int
             L.orc_processed_blocks.argtypes = [C.c_int, P, P]
             L.orc_processed_blocks.restype = C.c_uint64
             L.orc_lorenzo.argtypes = [P, C.c_int, P, P]
@@ -239,6 +244,37 @@ def estimate_paper(x: np.ndarray, eb: float, mode: str = "rel", stride=None,
     if st_ != 0:
         raise OracleError(st_)
     return res.to_dict()
+
+
+def zfp_stream(x: np.ndarray, eb: float, mode: str = "rel", stride=None):
+    """SURVEY 8(f) N3 (Alg. 1 line 13): the fixed-accuracy ZFP stream of the processed
+    blocks -> (bytes as uint8 array, length in bits)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    nd, dims, st = _dims_stride(x.shape, stride)
+    nbits = C.c_uint64()
+    m = 1 if mode == "rel" else 0
+    sp = None if st is None else _ptr(st)
+    rc = lib().orc_zfp_stream(_ptr(x), nd, _ptr(dims), m, float(eb), sp, None, 0, C.byref(nbits))
+    if rc != 0:
+        raise OracleError(rc)
+    buf = np.zeros(((nbits.value + 31) // 32) * 4, np.uint8)
+    rc = lib().orc_zfp_stream(_ptr(x), nd, _ptr(dims), m, float(eb), sp, _ptr(buf), buf.size, C.byref(nbits))
+    if rc != 0:
+        raise OracleError(rc)
+    return buf, int(nbits.value)
+
+
+def zfp_stream_decode(buf: np.ndarray, nbits: int, shape, eb: float, value_range: float, mode: str = "rel",
+                      stride=None) -> np.ndarray:
+    """Decode a zfp_stream back to float32 values (processed blocks; others 0)."""
+    nd, dims, st = _dims_stride(tuple(shape), stride)
+    out = np.zeros(shape, np.float32)
+    b = np.ascontiguousarray(buf, dtype=np.uint8)
+    rc = lib().orc_zfp_stream_decode(_ptr(b), int(nbits), nd, _ptr(dims), 1 if mode == "rel" else 0, float(eb),
+                                     float(value_range), None if st is None else _ptr(st), _ptr(out))
+    if rc != 0:
+        raise OracleError(rc)
+    return out
 
 
 def paper_positions(nd: int) -> np.ndarray:

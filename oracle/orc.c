@@ -832,3 +832,153 @@ int orc_estimate_paper(const float *x, int nd, const int64_t *dims, int eb_mode,
   free(hist);
   return rc;
 }
+
+/* ------------------------------------------------------------------ */
+/* the fixed-accuracy ZFP stream (Alg. 1 line 13)       */
+/* ------------------------------------------------------------------ */
+static void put_bits(uint8_t *buf, uint64_t *pos, uint64_t cap_bits, uint32_t v, int n) {
+  for (int i = 0; i < n; ++i) {
+    if (*pos < cap_bits) put_bit(buf, *pos, (int)((v >> i) & 1u));
+    ++*pos;
+  }
+}
+
+/* derived scalars of Alg. 1 line 2 (A1/A2) for the stream routines */
+static int stream_setup(const float *x, int nd, const int64_t *dims, int eb_mode, double eb, double *VR,
+                        int32_t *minexp) {
+  int64_t N = 1;
+  for (int a = 0; a < nd; ++a) { if (dims[a] < 1) return ORC_EINVAL; N *= dims[a]; }
+  if (!isfinite(eb) || !(eb > 0.0) || (eb_mode != 0 && eb_mode != 1)) return ORC_EINVAL;
+  if (x) {
+    float vmin = x[0], vmax = x[0];
+    for (int64_t i = 0; i < N; ++i) {
+      if (!isfinite(x[i])) return ORC_ENONFINITE;
+      if (x[i] < vmin) vmin = x[i];
+      if (x[i] > vmax) vmax = x[i];
+    }
+    *VR = (double)vmax - (double)vmin;
+  }
+  const double eb_abs = eb_mode == 1 ? eb * *VR : eb;
+  if (eb_mode == 1 && *VR == 0.0) return ORC_EDEGENERATE;
+  if (!(eb_abs > 0.0)) return ORC_EINVAL;
+  int fe; frexp(eb_abs, &fe);
+  *minexp = fe - 1;
+  return ORC_OK;
+}
+
+int orc_zfp_stream(const float *x, int nd, const int64_t *dims, int eb_mode, double eb,
+                   const int32_t *stride, uint8_t *buf, uint64_t cap_bytes, uint64_t *nbits) {
+  if (nd < 1 || nd > 3 || !x || !dims || !nbits) return ORC_EINVAL;
+  double VR = 0.0;
+  int32_t minexp = 0;
+  int rc = stream_setup(x, nd, dims, eb_mode, eb, &VR, &minexp);
+  if (rc) return rc;
+  int32_t s[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) s[a] = stride ? stride[a] : 1;
+  const int size = (int)ipow4(nd);
+  int32_t perm[64];
+  orc_sequency_perm(nd, perm);
+  int64_t nb[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) nb[a] = (dims[a] + 3) / 4;
+  const uint64_t cap_bits = buf ? cap_bytes * 8 : 0;
+  if (buf) memset(buf, 0, cap_bytes);
+  uint8_t ec[64 * 33 / 8 + 64];                 /* one block's EC bits (<= 32 x (64 + 1) bits) */
+  uint64_t pos = 0;
+  for (int64_t lb = 0; lb < nb[0] * nb[1] * nb[2]; ++lb) {
+    int64_t b[3], r = lb;
+    for (int a = nd - 1; a >= 0; --a) { b[a] = r % nb[a]; r /= nb[a]; }
+    int processed = 1;
+    for (int a = 0; a < nd; ++a) if (b[a] % s[a] != 0) processed = 0;
+    if (!processed) continue;
+    float blk[64];
+    for (int n = 0; n < size; ++n) {
+      int64_t cl[3];
+      int rr = n;
+      for (int a = nd - 1; a >= 0; --a) {
+        const int64_t i = 4 * b[a] + rr % 4;
+        rr /= 4;
+        cl[a] = i < dims[a] ? i : dims[a] - 1;        /* edge replication (R17) */
+      }
+      int64_t lin = 0;
+      for (int a = 0; a < nd; ++a) lin = lin * dims[a] + cl[a];
+      blk[n] = x[lin];
+    }
+    const int32_t emax = orc_block_emax(blk, size);
+    if (emax == -127) { put_bits(buf, &pos, cap_bits, 0u, 1); continue; }   /* empty block */
+    int32_t coef[64];
+    uint32_t u[64];
+    orc_block_bfp(blk, size, emax, coef);
+    orc_fwd_xform(coef, nd);
+    for (int j = 0; j < size; ++j) u[j] = orc_negabinary(coef[perm[j]]);
+    const int32_t p = orc_precision(emax, minexp, nd);
+    if (p == 0) { put_bits(buf, &pos, cap_bits, 0u, 1); continue; }      /* nothing kept */
+    put_bits(buf, &pos, cap_bits, 1u, 1);
+    put_bits(buf, &pos, cap_bits, (uint32_t)(emax + 127), 8);
+    memset(ec, 0, sizeof ec);
+    const uint64_t n = orc_gt_encode(u, size, 32 - p, ec, sizeof(ec) * 8);
+    for (uint64_t i = 0; i < n; ++i) {
+      if (pos < cap_bits) put_bit(buf, pos, get_bit(ec, i));
+      ++pos;
+    }
+  }
+  *nbits = pos;
+  return (buf && pos > cap_bits) ? ORC_EINVAL : ORC_OK;
+}
+
+int orc_zfp_stream_decode(const uint8_t *buf, uint64_t nbits, int nd, const int64_t *dims, int eb_mode,
+                          double eb, double VR, const int32_t *stride, float *out) {
+  if (nd < 1 || nd > 3 || !buf || !dims || !out) return ORC_EINVAL;
+  int32_t minexp = 0;
+  int rc = stream_setup(NULL, nd, dims, eb_mode, eb, &VR, &minexp);
+  if (rc) return rc;
+  int32_t s[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) s[a] = stride ? stride[a] : 1;
+  const int size = (int)ipow4(nd);
+  int32_t perm[64];
+  orc_sequency_perm(nd, perm);
+  int64_t nb[3] = {1, 1, 1};
+  for (int a = 0; a < nd; ++a) nb[a] = (dims[a] + 3) / 4;
+  uint64_t pos = 0;
+  for (int64_t lb = 0; lb < nb[0] * nb[1] * nb[2]; ++lb) {
+    int64_t b[3], r = lb;
+    for (int a = nd - 1; a >= 0; --a) { b[a] = r % nb[a]; r /= nb[a]; }
+    int processed = 1;
+    for (int a = 0; a < nd; ++a) if (b[a] % s[a] != 0) processed = 0;
+    if (!processed) continue;
+    float blk[64];
+    if (pos >= nbits) return ORC_EINVAL;
+    if (!get_bit(buf, pos++)) {
+      for (int n = 0; n < size; ++n) blk[n] = 0.0f;   /* empty or p = 0: decodes to zeros */
+    } else {
+      uint32_t e8 = 0;
+      for (int i = 0; i < 8; ++i) e8 |= (uint32_t)get_bit(buf, pos++) << i;
+      const int32_t emax = (int32_t)e8 - 127;
+      const int kmin = 32 - orc_precision(emax, minexp, nd);
+      /* the EC bits: decode from a copy starting at bit 0 */
+      uint8_t ec[64 * 33 / 8 + 64];
+      memset(ec, 0, sizeof ec);
+      const uint64_t avail = nbits - pos < sizeof(ec) * 8 ? nbits - pos : sizeof(ec) * 8;
+      for (uint64_t i = 0; i < avail; ++i) put_bit(ec, i, get_bit(buf, pos + i));
+      uint32_t u[64];
+      pos += orc_gt_decode(ec, avail, size, kmin, u);
+      int32_t coef[64];
+      for (int j = 0; j < size; ++j) coef[perm[j]] = orc_negabinary_inv(u[j]);
+      orc_inv_xform(coef, nd);
+      for (int n = 0; n < size; ++n) blk[n] = (float)ldexp((double)coef[n], emax - 30);
+    }
+    for (int n = 0; n < size; ++n) {
+      int64_t idx[3];
+      int inside = 1, rr = n;
+      for (int a = nd - 1; a >= 0; --a) {
+        idx[a] = 4 * b[a] + rr % 4;
+        rr /= 4;
+        if (idx[a] >= dims[a]) inside = 0;
+      }
+      if (!inside) continue;
+      int64_t lin = 0;
+      for (int a = 0; a < nd; ++a) lin = lin * dims[a] + idx[a];
+      out[lin] = blk[n];
+    }
+  }
+  return pos == nbits ? ORC_OK : ORC_EINVAL;
+}

@@ -108,6 +108,20 @@ int orc_paper_positions(int ndims, int32_t *pos);
 void orc_block_paper(const uint32_t *u_seq, int ndims, int kmin, int32_t emax, uint64_t *nsb2,
                      double *mse_num);
 
+/* ---- Alg. 1 line 13, "perform ZFP compression on X_i with absolute
+ * error bound eb" -- the fixed-accuracy stream whose per-block lengths the estimator counts
+ * (P:436).  Per processed block, row-major: 1 bit 0 if the block is
+ * empty or p = 0; else 1 bit 1, 8 bits emax + 127 (LSB first), then the group-testing
+ * embedded code of planes 31..kmin (orc_gt_encode).  Bits are packed LSB first within
+ * bytes.  Returns ORC_OK and the stream length in *nbits; ORC_EINVAL if cap_bytes is too
+ * small (with *nbits = the length needed). */
+int orc_zfp_stream(const float *x, int ndims, const int64_t *dims, int eb_mode, double eb,
+                   const int32_t *stride, uint8_t *buf, uint64_t cap_bytes, uint64_t *nbits);
+/* decode such a stream into the field (processed blocks only; other values untouched):
+ * words -> negabinary inverse -> sequency inverse -> inverse lift -> x 2^(emax-30) */
+int orc_zfp_stream_decode(const uint8_t *buf, uint64_t nbits, int ndims, const int64_t *dims, int eb_mode,
+                          double eb, double value_range, const int32_t *stride, float *out);
+
 /* ---- single steps, exported for the pin tests ---- */
 float orc_lorenzo(const float *x, int ndims, const int64_t *dims, const int64_t *idx);
 int32_t orc_quantize(float d, float r_f);

@@ -769,3 +769,49 @@ def test_paper_sampled_blocks(orc):
     nb = orc.processed_blocks(x.shape, (1, 10))
     assert r["n_samples"] == 9 * nb
     assert r["hist_total"] == 16 * nb - 1          # every real point but the origin
+
+
+# ------------------------------------------------------ N3: the ZFP stream (Alg. 1 line 13)
+def _stream_cases():
+    import synth
+    return [("c1", synth.c1_field(), 1e-4, None), ("c1-loose", synth.c1_field(), 1e-2, None),
+            ("c3", synth.c3_field(0, shape=(37, 45, 70)), 1e-3, None),
+            ("c3-zeros", synth.c3_field(5, shape=(37, 45, 70)), 1e-5, None),
+            ("c5-noise", synth.c5_field(2, shape=(32, 48, 64)), 1e-6, None),
+            ("c4", synth.c4_field(0, shape=(64, 64, 64)), 1e-4, None),
+            ("c2-sampled", synth.c2_field(3, shape=(120, 400)), 1e-4, (1, 10)),
+            ("1d-odd", np.cumsum(np.random.default_rng(1).standard_normal(10001)).astype(np.float32), 1e-3, None)]
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_zfp_stream_length_and_accuracy(orc, i):
+    """The stream ACTUALLY written for Alg. 1 line 13 (fixed accuracy at eb) has
+    exactly the length the estimator counted (sum of per-block header + EC bits, A13/A15),
+    decodes within the error bound (max |x - x^| <= eb_abs), and its real MSE is within
+    +-10 % of the gain-weighted estimate (A14; the literal unit-weight reading is >4x off)."""
+    name, x, eb, stride = _stream_cases()[i]
+    r = orc.estimate(x, eb, stride=stride)
+    buf, nbits = orc.zfp_stream(x, eb, stride=stride)
+    assert nbits == r["zfp_total_bits"], name
+    y = orc.zfp_stream_decode(buf, nbits, x.shape, eb, r["value_range"], stride=stride)
+    if stride is None:
+        err = np.abs(y.astype(np.float64) - x)
+        assert err.max() <= r["eb_abs"], (name, err.max(), r["eb_abs"])
+        mse = float((err ** 2).mean())
+        if r["zfp_mse"] > 0:
+            assert 0.9 <= mse / r["zfp_mse"] <= 1.1, (name, mse, r["zfp_mse"])
+        else:
+            assert mse == 0.0
+
+
+def test_zfp_stream_empty_and_constant(orc):
+    """All-zero field: one 0 bit per block.  Constant block: header + the A15 closed form."""
+    z = np.zeros((8, 12), np.float32)
+    buf, nbits = orc.zfp_stream(z, 1e-3, mode="abs")
+    assert nbits == 6 and not buf.any()
+    c = np.full((4, 4, 4), 3.0, np.float32)
+    buf, nbits = orc.zfp_stream(c, 1e-3, mode="abs")
+    r = orc.estimate(c, 1e-3, mode="abs")
+    assert nbits == r["zfp_total_bits"]
+    y = orc.zfp_stream_decode(buf, nbits, c.shape, 1e-3, r["value_range"], mode="abs")
+    assert np.abs(y - c).max() <= 1e-3
