@@ -148,6 +148,21 @@ int sel_set_option(sel_plan_t plan, const char *key, double value);
  * Errors: SEL_EINVAL, SEL_ENONFINITE, SEL_EDEGENERATE, SEL_ECUDA. */
 int sel_estimate(sel_plan_t plan, const float *d_field, void *stream, sel_result *out);
 
+/* N3: the ZFP branch of Alg. 1 lines 11-15 -- "perform ZFP
+ * compression on X_i with absolute error bound eb": the fixed-accuracy ZFP stream of the
+ * plan's processed blocks (stride 1: the whole field), whose per-block lengths are the
+ * bits the estimate counts (zfp_total_bits == *nbits).  Per block, row-major: 1 bit 0 if
+ * the block is empty or keeps no bit plane; else 1 bit 1, 8 bits emax + 127, then the
+ * group-testing embedded code of planes 31..kmin (R13); bits packed
+ * LSB first into little-endian 32-bit words.
+ *   d_out : device buffer owned by the caller, or NULL to query the length only;
+ *           cap_bytes must be >= ceil(*nbits / 32) * 4 (else SEL_EINVAL, *nbits set).
+ *   nbits : out, the stream length in bits.
+ * Synchronises `stream`.  The SZ branch (line 12) is not built.
+ * Errors: SEL_EINVAL, SEL_ENONFINITE, SEL_EDEGENERATE, SEL_ENOMEM, SEL_ECUDA. */
+int sel_compress_zfp(sel_plan_t plan, const float *d_field, void *d_out, uint64_t cap_bytes, uint64_t *nbits,
+                     void *stream);
+
 /* N2: the paper-literal estimate of one device field with the plan's eb,
  * mode and stride (sel_paper_result above).  Two dependent passes, as Alg. 1 prints them:
  * the ZFP samples give PSNR_sp, whose delta fixes the SZ re-quantisation of the same

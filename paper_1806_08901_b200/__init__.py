@@ -24,6 +24,7 @@ EB_ABS, EB_REL = 0, 1
 
 # every entry point declared in include/sel.h
 EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_multi", "sel_estimate_paper",
+           "sel_compress_zfp",
            "sel_estimate_batch",
            "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_choose_eb",
            "sel_debug_copy", "sel_batch_layout", "sel_kernel_times",
@@ -89,6 +90,8 @@ def lib():
         L.sel_set_option.restype = C.c_int
         L.sel_estimate.argtypes = [P, P, P, C.POINTER(Result)]
         L.sel_estimate.restype = C.c_int
+        L.sel_compress_zfp.argtypes = [P, P, P, C.c_uint64, C.POINTER(C.c_uint64), P]
+        L.sel_compress_zfp.restype = C.c_int
         L.sel_estimate_paper.argtypes = [P, P, P, C.POINTER(PaperResult)]
         L.sel_estimate_paper.restype = C.c_int
         L.sel_estimate_multi.argtypes = [P, P, C.c_int, P, P, P]
@@ -242,6 +245,19 @@ class Plan:
         _check(lib().sel_estimate(self._h, C.c_void_p(_device_ptr(field, self.shape, self.device)), _stream_ptr(stream),
                                   C.byref(r)))
         return r.to_dict()
+
+    def compress_zfp(self, field, stream=None):
+        """N3 (Alg. 1 line 13): the fixed-accuracy ZFP stream of `field` at the plan's eb
+        (sel_compress_zfp) -> (uint8 CUDA tensor of the stream bytes, length in bits)."""
+        import torch
+        ptr = C.c_void_p(_device_ptr(field, self.shape, self.device))
+        nbits = C.c_uint64()
+        _check(lib().sel_compress_zfp(self._h, ptr, None, 0, C.byref(nbits), _stream_ptr(stream)))
+        nbytes = (nbits.value + 31) // 32 * 4
+        out = torch.empty(max(nbytes, 4), dtype=torch.uint8, device=field.device)
+        _check(lib().sel_compress_zfp(self._h, ptr, C.c_void_p(out.data_ptr()), out.numel(), C.byref(nbits),
+                                      _stream_ptr(stream)))
+        return out[:nbytes], int(nbits.value)
 
     def estimate_paper(self, field, stream=None) -> dict:
         """N2: the paper-literal estimate (sel_estimate_paper): sampled-coefficient n_sb

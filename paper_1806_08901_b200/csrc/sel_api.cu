@@ -111,6 +111,8 @@ struct sel_plan_st {
   Partial *mpart = nullptr;                       // [kMultiMaxEb][mcap]
   int mcap = 0;                                   // CTA partials per eb
 
+  // N3 ZFP stream workspace (first use): per-block lengths, CTA bases, total
+  void *zs_mem = nullptr;
   // N2 paper-literal workspace (first use): CTA partials, mid scalars, params, result
   void *paper_mem = nullptr;
   int paper_cap = 0;
@@ -661,6 +663,45 @@ int sel_estimate(sel_plan_t p, const float *d_field, void *stream, sel_result *o
   return SEL_OK;
 }
 
+int sel_compress_zfp(sel_plan_t p, const float *d_field, void *d_out, uint64_t cap_bytes, uint64_t *nbits,
+                     void *stream) {
+  if (!p || !d_field || !nbits || p->timing || p->debug) return SEL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t wsb = zstream_ws_bytes(p->geo.n_pb);
+  if (!p->zs_mem) {
+    if (cudaMalloc(&p->zs_mem, wsb + 256) != cudaSuccess) {
+      cudaGetLastError();
+      p->zs_mem = nullptr;
+      return SEL_ENOMEM;
+    }
+  }
+  unsigned long long *d_total = (unsigned long long *)((char *)p->zs_mem + ((wsb + 127) & ~(size_t)127));
+  Geo g = p->geo;
+  g.vec = (g.n[2] % 4 == 0) && (((uintptr_t)d_field & 15u) == 0);
+  const Workspace w0 = field_ws(p, 0);
+  int rc = launch_minmax(d_field, g.N, p->mm_ctas, w0, p->mode, p->eb, st);   // Alg. 1 line 2
+  if (rc) return cuda_fail(cudaGetLastError(), "k_minmax launch");
+  if ((rc = launch_zstream_bits(d_field, g, p->sm_count, w0.params, p->zs_mem, d_total, st)))
+    return cuda_fail(cudaGetLastError(), "stream length launch");
+  unsigned long long total = 0;
+  Params prm;
+  CK(cudaMemcpyAsync(&total, d_total, sizeof(total), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&prm, w0.params, sizeof(prm), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  p->launches += 4;
+  if (prm.status != SEL_OK) return prm.status;
+  *nbits = total;
+  if (!d_out) return SEL_OK;                                  // size query
+  const uint64_t bytes = (total + 31) / 32 * 4;
+  if (cap_bytes < bytes) return SEL_EINVAL;
+  CK(cudaMemsetAsync(d_out, 0, bytes, st));
+  if ((rc = launch_zstream_write(d_field, g, w0.params, p->zs_mem, (uint32_t *)d_out, st)))
+    return cuda_fail(cudaGetLastError(), "stream write launch");
+  p->launches += 1;
+  CK(cudaStreamSynchronize(st));
+  return SEL_OK;
+}
+
 int sel_estimate_paper(sel_plan_t p, const float *d_field, void *stream, sel_paper_result *out) {
   if (!p || !d_field || !out || p->timing || p->debug) return SEL_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -949,6 +990,7 @@ void sel_plan_destroy(sel_plan_t p) {
   if (p->ws_mem) cudaFree(p->ws_mem);
   if (p->multi_mem) cudaFree(p->multi_mem);
   if (p->paper_mem) cudaFree(p->paper_mem);
+  if (p->zs_mem) cudaFree(p->zs_mem);
   if (p->d_res) cudaFree(p->d_res);
   if (p->h_res) cudaFreeHost(p->h_res);
   if (p->dbg_mem) cudaFree(p->dbg_mem);

@@ -165,6 +165,11 @@ int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Worksp
 int launch_finalize(const Workspace &ws, const FinalizeArgs &fa, sel_result *d_out,
                     unsigned long long *dbg_hist, cudaStream_t st);
 int minmax_ctas(int64_t N, int sm_count);
+// N3 ZFP stream (sel_stream.cu)
+size_t zstream_ws_bytes(int64_t n_pb);
+int launch_zstream_bits(const float *x, const Geo &g, int sm_count, const Params *prm, void *ws,
+                        unsigned long long *d_total, cudaStream_t st);
+int launch_zstream_write(const float *x, const Geo &g, const Params *prm, void *ws, uint32_t *out, cudaStream_t st);
 // N2 paper-literal estimator (sel_paper.cu)
 size_t paper_ws_bytes(int max_ctas);
 int launch_paper_zfp(const float *x, const Geo &g, int sm_count, int max_ctas, const Params *base, void *pws,

@@ -729,3 +729,65 @@ def test_paper_estimator_errors(sel):
         with pytest.raises(sel.SelError) as e:
             p.estimate_paper(bad)
         assert e.value.status == sel.SEL_ENONFINITE
+
+
+# ---------------------------------------------------------------- N3: the ZFP stream
+@pytest.mark.parametrize("case", ["c1", "c2r", "c2s", "c3r", "c3z", "c4", "c5", "odd1d", "odd3d", "zeros"])
+def test_zfp_stream_vs_oracle(sel, orc, case):
+    """sel_compress_zfp (Alg. 1 line 13) writes the oracle's stream BIT FOR BIT, its length
+    is the estimate's zfp_total_bits, and the oracle decodes it within the error bound."""
+    import synth
+    mode, stride, eb = "rel", None, 1e-4
+    if case == "c1":
+        x = synth.c1_field()
+    elif case == "c2r":
+        x = synth.c2_field(0, shape=(203, 516))
+    elif case == "c2s":
+        x, stride = synth.c2_field(3, shape=(120, 400)), (1, 10)
+    elif case == "c3r":
+        x, eb = synth.c3_field(2, shape=(37, 45, 70)), 1e-3
+    elif case == "c3z":
+        x, eb = synth.c3_field(5, shape=(37, 45, 70)), 1e-5
+    elif case == "c4":
+        x = synth.c4_field(0, shape=(64, 64, 64))
+    elif case == "c5":
+        x, eb = synth.c5_field(2, shape=(32, 48, 64)), 1e-6
+    elif case == "odd1d":
+        x = np.cumsum(np.random.default_rng(3).standard_normal(10007)).astype(np.float32)
+    elif case == "odd3d":
+        x = np.cumsum(np.random.default_rng(4).standard_normal((9, 14, 21)), axis=2).astype(np.float32)
+    else:
+        x, eb, mode = np.zeros((16, 20), np.float32), 1e-3, "abs"
+    ref, nref = orc.zfp_stream(x, eb, mode=mode, stride=stride)
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    with sel.Plan(x.shape, eb, mode, stride) as p:
+        buf, nbits = p.compress_zfp(t)
+        if case != "zeros":
+            r = p.estimate(t)
+            assert nbits == r["zfp_total_bits"]
+    assert nbits == nref
+    got = buf.cpu().numpy()
+    nb = (nbits + 7) // 8
+    assert np.array_equal(got[:nb], ref[:nb]), case
+    if stride is None and case != "zeros":
+        o = orc.estimate(x, eb, mode=mode)
+        y = orc.zfp_stream_decode(got, nbits, x.shape, eb, o["value_range"], mode=mode)
+        assert np.abs(y.astype(np.float64) - x).max() <= o["eb_abs"]
+
+
+def test_zfp_stream_full_size(sel, orc):
+    """C4 field 2 (512^3, 2.1 M blocks): the stream equals the oracle's bit for bit."""
+    import synth
+    x = synth.c4_field(2)
+    ref, nref = orc.zfp_stream(x, 1e-4)
+    with sel.Plan(x.shape, 1e-4) as p:
+        buf, nbits = p.compress_zfp(torch.from_numpy(x).cuda())
+    assert nbits == nref
+    assert np.array_equal(buf.cpu().numpy()[: (nbits + 7) // 8], ref[: (nbits + 7) // 8])
+
+
+def test_zfp_stream_errors(sel):
+    with sel.Plan((8, 8), 1e-3) as p:
+        with pytest.raises(sel.SelError) as e:
+            p.compress_zfp(torch.ones(8, 8, device="cuda"))
+        assert e.value.status == sel.SEL_EDEGENERATE
