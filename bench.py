@@ -482,6 +482,38 @@ def main():
               "ms_per_step": rms, "entry": "sel_estimate_multi per field (k_minmax + k_multi + k finalizes)"}
         mp.close()
 
+    # ---- SURVEY 8(f) N2 / N3 on the same fields: the paper-literal estimate (Alg. 1 as
+    # printed; its choices next to the exact ones) and the ZFP stream of Alg. 1 line 13
+    paper_line, stream_line = None, None
+    if not args.no_rd:
+        pp = sel.Plan(shape, eb, "rel", st)
+        pp.estimate_paper(dfields[0])
+        torch.cuda.synchronize()
+        q0 = time.perf_counter()
+        pres = [pp.estimate_paper(f) for f in dfields]
+        torch.cuda.synchronize()
+        pdt = time.perf_counter() - q0
+        agree = sum(1 for a, b in zip(pres, results) if a["choice"] == b["choice"])
+        paper_line = {"value": field_bytes / pdt / 1e9, "unit": "GB/s", "clock": "host wall (per-field sync calls)",
+                      "choices_equal_to_exact": f"{agree}/{nf}",
+                      "zfp_nsb_bits": [round(r["zfp_nsb_bits"], 4) for r in pres],
+                      "zfp_psnr_sp": [round(r["zfp_psnr_sp"], 2) for r in pres],
+                      "sz_bits_at_delta": [round(r["sz_bits"], 4) for r in pres]}
+        if min(st) == 1:
+            pp.compress_zfp(dfields[0])
+            torch.cuda.synchronize()
+            q0 = time.perf_counter()
+            tot_bits = 0
+            for f in dfields:
+                _, nb_ = pp.compress_zfp(f)
+                tot_bits += nb_
+            torch.cuda.synchronize()
+            sdt = time.perf_counter() - q0
+            stream_line = {"value": field_bytes / sdt / 1e9, "unit": "GB/s", "clock": "host wall (per-field sync calls)",
+                           "bits_per_value": tot_bits / (nf * int(np.prod(shape))),
+                           "entry": "sel_compress_zfp (lengths + scan + write)"}
+        pp.close()
+
     if rank != 0:
         barrier(world)
         return 0
@@ -527,7 +559,8 @@ def main():
                    "fields_per_s": fields_per_s,
                    "pct_of_hbm_peak": 100.0 * value / (peak * world),
                    "sz_chosen": n_sz, "zfp_chosen": nf - n_sz,
-                   "sampled_mode": alt, "rd_curve": rd},
+                   "sampled_mode": alt, "rd_curve": rd, "paper_mode": paper_line,
+                   "zfp_stream": stream_line},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": names[dom],
                      "peak_source": peak_kind,

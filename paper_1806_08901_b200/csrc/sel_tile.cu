@@ -8,10 +8,10 @@
 // cp.async.bulk.tensor (TMA) per task, completing on an mbarrier (expect_tx).  TMA's
 // out-of-bounds zero fill IS the Lorenzo zero boundary (P:151 footnote; reading R4), so
 // the consumer code has no boundary branches.  Consumers compute the SZ residuals (nested
-// first differences, R4) and quantisation codes (R5) from shared memory into a
-// lane-replicated shared-memory histogram window (C copies: a smooth field sends all 32
-// lanes to the same code, and copies turn a 32-way same-address conflict into a
-// 32/C-way one), then each lane runs the ZFP block pipeline (zfp_block, R8-R14) on its
+// first differences, R4) and quantisation codes (R5) from shared memory into one CTA-wide
+// shared-memory histogram window (atomicAdd with an unused result compiles to
+// ATOMS.POPC.INC, which merges the lanes of a warp hitting the same bin), then each lane
+// runs the ZFP block pipeline (zfp_block, R8-R14) on its
 // block, re-read from shared memory with the far-edge replication (R17) folded into the
 // row/plane index.  Every (task, warp) writes one partial, summed in task order by the
 // finalize kernel: bit-reproducible regardless of the dynamic schedule.
