@@ -9,6 +9,30 @@ CPU tests).
 from __future__ import annotations
 
 
+def setup(backend: str = "nccl"):
+    """(world, rank, local_rank) from the torchrun environment; initialises the process
+    group when world > 1 (NCCL on GPUs, one process per GPU; gloo in the CPU tests)."""
+    import os
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return world, rank, local
+
+
+def barrier() -> None:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.barrier()
+
+
 def shard(n_fields: int, rank: int, world: int) -> range:
     """Contiguous, balanced share of fields [0, n_fields) for `rank`."""
     if world < 1 or not 0 <= rank < world:

@@ -36,6 +36,7 @@ def _worker(rank, world, port, n_fields, q):
             local[i] = (r["choice"], r["sz_bits_per_value"], r["zfp_bits_per_value"])
         merged = sd.gather_results(local)
         tmax = sd.max_over_ranks(float(rank + 1))
+        sd.barrier()
         if rank == 0:
             q.put((merged, tmax))
     finally:
