@@ -111,6 +111,9 @@ struct sel_plan_st {
   Partial *mpart = nullptr;                       // [kMultiMaxEb][mcap]
   int mcap = 0;                                   // CTA partials per eb
 
+  // small-field single-launch state (first use)
+  void *small_mem = nullptr;
+  int use_small = 1;              // option "small_kernel"
   // N3 ZFP stream workspace (first use): per-block lengths, CTA bases, total
   void *zs_mem = nullptr;
   // N2 paper-literal workspace (first use): CTA partials, mid scalars, params, result
@@ -315,6 +318,37 @@ int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st,
   if (rc) return rc;
   p->launches += 1;
   p->batch_timed = p->timing;
+  return SEL_OK;
+}
+
+// one small field (N <= 2^21): one cooperative launch, k_small (sel_kernels.cu)
+bool small_ok(sel_plan_t p) {
+  return p->use_small && p->use_batch && !p->timing && !p->debug && p->geo.N <= ((int64_t)1 << 21);
+}
+
+int enqueue_small(sel_plan_t p, const float *d_field, cudaStream_t st) {
+  int rc;
+  if (!p->small_mem) {
+    if (cudaMalloc(&p->small_mem, small_state_bytes(p->sm_count)) != cudaSuccess) {
+      cudaGetLastError();
+      p->small_mem = nullptr;
+      return SEL_ENOMEM;
+    }
+    if ((rc = init_small_state(p->small_mem, st))) return cuda_fail(cudaGetLastError(), "small state");
+  }
+  Geo g = p->geo;
+  g.vec = (g.n[2] % 4 == 0) && (((uintptr_t)d_field & 15u) == 0);
+  FinalizeArgs fa;
+  fa.mode = p->mode;
+  fa.eb = p->eb;
+  fa.sz_offset = p->sz_offset;
+  fa.n_sz = p->n_sz;
+  fa.n_values = p->n_values;
+  fa.n_blocks = (uint64_t)p->geo.n_pb;
+  fa.ntasks = 0;
+  if ((rc = launch_small(d_field, g, p->sm_count, p->small_mem, field_ws(p, 0), fa, p->d_res, st)))
+    return cuda_fail(cudaGetLastError(), "k_small launch");
+  p->launches += 1;
   return SEL_OK;
 }
 
@@ -630,6 +664,10 @@ int sel_set_option(sel_plan_t p, const char *key, double value) {
     p->batch_debug = value != 0.0;
     return SEL_OK;
   }
+  if (!strcmp(key, "small_kernel")) {
+    p->use_small = value != 0.0;
+    return SEL_OK;
+  }
   if (!strcmp(key, "batch_kernel")) {
     p->use_batch = value != 0.0;
     return SEL_OK;
@@ -651,7 +689,9 @@ int sel_estimate(sel_plan_t p, const float *d_field, void *stream, sel_result *o
   int rc = ensure_results(p, 1);
   if (rc) return rc;
   if (p->timing && (rc = ensure_timing(p, 1))) return rc;
-  if (batch_ok(p, &d_field, 1)) {
+  if (small_ok(p)) {
+    if ((rc = enqueue_small(p, d_field, st))) return rc;
+  } else if (batch_ok(p, &d_field, 1)) {
     if ((rc = enqueue_batch(p, &d_field, 1, st))) return rc;
   } else if ((rc = enqueue_field(p, d_field, st, 0))) {
     return rc;
@@ -828,7 +868,9 @@ int sel_estimate_batch_async(sel_plan_t p, const float *const *d_fields, int n, 
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_results(p, n);
   if (rc) return rc;
-  if (batch_ok(p, d_fields, n)) {
+  if (n == 1 && small_ok(p)) {
+    if ((rc = enqueue_small(p, d_fields[0], st))) return rc;
+  } else if (batch_ok(p, d_fields, n)) {
     if ((rc = enqueue_batch(p, d_fields, n, st))) return rc;
   } else if (n >= 2 && p->pipeline) {
     if ((rc = enqueue_pipelined(p, d_fields, n, st))) return rc;
@@ -927,6 +969,12 @@ int sel_choose_eb(const sel_result *r, int32_t *choice) {
 }
 
 int sel_debug_copy(sel_plan_t p, const char *what, void *dst, uint64_t bytes) {
+  if (p && what && !strcmp(what, "small_prof")) {   // developer probe (SEL_SMALL_PROF builds)
+    if (!p->small_mem || !dst || bytes != 7 * 8) return SEL_EINVAL;
+    const size_t off = 256 + (size_t)p->sm_count * (sizeof(Partial) + 24);
+    CK(cudaMemcpy(dst, (char *)p->small_mem + off, bytes, cudaMemcpyDeviceToHost));
+    return SEL_OK;
+  }
   if (!p || !what || !dst) return SEL_EINVAL;
   if (!strncmp(what, "batch_", 6)) {     // k_batch dumps of the last batch launch
     if (!p->bdump.hist || p->last_batch_nf < 1 || p->last_batch_nf > p->bdump_cap) return SEL_EINVAL;
@@ -991,6 +1039,7 @@ void sel_plan_destroy(sel_plan_t p) {
   if (p->multi_mem) cudaFree(p->multi_mem);
   if (p->paper_mem) cudaFree(p->paper_mem);
   if (p->zs_mem) cudaFree(p->zs_mem);
+  if (p->small_mem) cudaFree(p->small_mem);
   if (p->d_res) cudaFree(p->d_res);
   if (p->h_res) cudaFreeHost(p->h_res);
   if (p->dbg_mem) cudaFree(p->dbg_mem);

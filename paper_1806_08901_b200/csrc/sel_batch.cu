@@ -43,6 +43,12 @@ constexpr int kH32Stride = kNSlots + 4;
 #ifndef SEL_CLAIM
 #define SEL_CLAIM 1                            // producer: task ids claimed per atomic
 #endif
+#ifndef SEL_PWAIT
+#define SEL_PWAIT 1000                          // producer stage wait: 0 probe loop, > 0 try_wait hint (ns)
+#endif
+#ifndef SEL_RSLEEP
+#define SEL_RSLEEP 32                          // release warp: first / reset sleep between queue polls (ns)
+#endif
 #ifndef SEL_PBACKOFF
 #define SEL_PBACKOFF 64                        // producer: longest sleep between stage probes (ns)
 #endif
@@ -216,9 +222,23 @@ constexpr int kRelQ = 16;
 template <int D>
 constexpr int batch_threads() { return (TileCfg<D>::CW + 2) * 32; }   // + producer + release warp
 
-// producer: wait until a stage is free, sleeping with a short back-off (a tight probe
-// loop took ~7 % of the 3D kernel's issued instructions, ncu r01c)
+// producer: wait until a stage is free.  SEL_PWAIT = 0: probe + nanosleep back-off;
+// otherwise a hardware-suspended mbarrier.try_wait with that time hint (ns): the thread
+// sleeps until the phase completes (or the hint expires) instead of re-issuing probes --
+// the probe loop took ~8 % of the 3D kernel's issued instructions (ncu r02b)
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
+  if (SEL_PWAIT > 0) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITP_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITP_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(SEL_PWAIT)
+        : "memory");
+    return;
+  }
   unsigned int ns = 64;
   while (!mbar_test(bar, parity)) {
     __nanosleep(ns);
@@ -400,14 +420,14 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   if (warp == CW + 1) {
     if (lane == 0) {
       unsigned int t = 0;
-      unsigned int ns = 32;
+      unsigned int ns = SEL_RSLEEP;
       for (;;) {
         if (t == ld_acquire_cta(&s_qhead)) {
           __nanosleep(ns);
           if (ns < 2048) ns <<= 1;        // requests are rare; polling steals issue slots
           continue;
         }
-        ns = 32;
+        ns = SEL_RSLEEP;
         const RelReq r = s_q[t % kRelQ];
         if (r.kind == REQ_END) break;
         if (r.kind == REQ_T) {

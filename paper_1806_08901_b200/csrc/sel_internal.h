@@ -165,6 +165,11 @@ int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Worksp
 int launch_finalize(const Workspace &ws, const FinalizeArgs &fa, sel_result *d_out,
                     unsigned long long *dbg_hist, cudaStream_t st);
 int minmax_ctas(int64_t N, int sm_count);
+// small single field in one cooperative launch (sel_kernels.cu)
+size_t small_state_bytes(int sm_count);
+int init_small_state(void *state, cudaStream_t st);
+int launch_small(const float *x, const Geo &g, int sm_count, void *state, const Workspace &ws,
+                 const FinalizeArgs &fa, sel_result *d_out, cudaStream_t st);
 // N3 ZFP stream (sel_stream.cu)
 size_t zstream_ws_bytes(int64_t n_pb);
 int launch_zstream_bits(const float *x, const Geo &g, int sm_count, const Params *prm, void *ws,

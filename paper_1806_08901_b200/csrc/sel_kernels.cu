@@ -321,12 +321,102 @@ __global__ void __launch_bounds__(256, (D == 3 ? SEL_MARCH3_MINB : 3)) k_march(c
 }
 
 // ============================================================ K2b: generic pass (sampled, 1D)
+// One processed block t (row-major over processed blocks): SZ residuals of its real points
+// with neighbours from the full field (R4, R5: codes into the smem window sh_hist or the
+// global histogram), then the ZFP block (R8-R14).  Shared by k_estimate and k_small.
 template <int D, bool VEC, bool DBG>
-__global__ void __launch_bounds__(256) k_estimate(const float *__restrict__ x, Geo g,
-                                                  Workspace ws, DebugPtrs dbg) {
+__device__ __forceinline__ void block_estimate(const float *__restrict__ x, const Geo &g, int64_t t, float r_f,
+                                               int minexp, unsigned int *sh_hist, unsigned long long *gh,
+                                               unsigned int &ovf, const DebugPtrs &dbg, uint32_t &bits,
+                                               double &E) {
   constexpr int SZ = Tab<D>::SIZE;
   constexpr int PL = D == 3 ? 4 : 1;   // planes per block (axis 0 of the 3-axis view)
   constexpr int RW = D >= 2 ? 4 : 1;   // rows per block   (axis 1)
+  const int64_t p2 = t % g.npb[2];
+  const int64_t q = t / g.npb[2];
+  const int64_t p1 = q % g.npb[1];
+  const int64_t p0 = q / g.npb[1];
+  const int64_t I0 = 4 * p0 * g.s[0], J0 = 4 * p1 * g.s[1], K0 = 4 * p2 * g.s[2];
+
+  float blk[SZ];
+  float dprev[RW][4];
+  // ---------------- SZ: Lorenzo on original values, nested differences (R4)
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dprev[r][c] = 0.0f;
+  if (D == 3 && I0 > 0) {
+    float up[4], uh = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) up[c] = 0.0f;
+    if (J0 > 0) load_row<VEC>(x, g, I0 - 1, J0 - 1, K0, up, uh);
+    float d1up[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) d1up[c] = up[c] - (c ? up[c - 1] : uh);
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      float v[4], h;
+      load_row<VEC>(x, g, I0 - 1, J0 + r, K0, v, h);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float d1 = v[c] - (c ? v[c - 1] : h);
+        dprev[r][c] = d1 - d1up[c];
+        d1up[c] = d1;
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < PL; ++p) {
+    const int64_t i = I0 + p;
+    float d1up[4];
+    {
+      float up[4], uh = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) up[c] = 0.0f;
+      if (D >= 2 && J0 > 0) load_row<VEC>(x, g, i, J0 - 1, K0, up, uh);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) d1up[c] = up[c] - (c ? up[c - 1] : uh);
+    }
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int64_t j = J0 + r;
+      float v[4], h;
+      load_row<VEC>(x, g, i, j, K0, v, h);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        blk[(p * RW + r) * 4 + c] = v[c];
+        const float d1 = v[c] - (c ? v[c - 1] : h);
+        const float d2 = d1 - d1up[c];
+        d1up[c] = d1;
+        const float d = d2 - dprev[r][c];
+        dprev[r][c] = d2;
+        const int64_t k = K0 + c;
+        const bool real = (i < g.n[0]) && (j < g.n[1]) && (k < g.n[2]);
+        const bool origin = (i == 0) && (j == 0) && (k == 0);
+        sz_put<DBG>(d, r_f, real && !origin, sh_hist, gh, ovf,
+                    DBG ? dbg.codes + (i * g.n[1] + j) * g.n[2] + k : nullptr);
+      }
+    }
+  }
+  int emax;
+  int cf[SZ];
+  uint32_t u[SZ];
+  zfp_block<D, DBG>(blk, minexp, bits, E, emax, cf, u);
+  if constexpr (DBG) {
+    dbg.emax[t] = emax;
+    dbg.bits[t] = bits;
+    dbg.err[t] = E;
+#pragma unroll
+    for (int n = 0; n < SZ; ++n) {
+      dbg.coef[t * SZ + n] = cf[n];
+      dbg.uword[t * SZ + n] = u[n];
+    }
+  }
+}
+
+template <int D, bool VEC, bool DBG>
+__global__ void __launch_bounds__(256) k_estimate(const float *__restrict__ x, Geo g,
+                                                  Workspace ws, DebugPtrs dbg) {
   extern __shared__ unsigned int sh_hist[];
   hist_zero(sh_hist);
   grid_dep_wait();
@@ -342,90 +432,11 @@ __global__ void __launch_bounds__(256) k_estimate(const float *__restrict__ x, G
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   // static thread -> block mapping; the per-CTA partial is this CTA's "task"
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < g.n_pb; t += gstride) {
-    const int64_t p2 = t % g.npb[2];
-    const int64_t q = t / g.npb[2];
-    const int64_t p1 = q % g.npb[1];
-    const int64_t p0 = q / g.npb[1];
-    const int64_t I0 = 4 * p0 * g.s[0], J0 = 4 * p1 * g.s[1], K0 = 4 * p2 * g.s[2];
-
-    float blk[SZ];
-    float dprev[RW][4];
-    // ---------------- SZ: Lorenzo on original values, nested differences (R4)
-#pragma unroll
-    for (int r = 0; r < RW; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) dprev[r][c] = 0.0f;
-    if (D == 3 && I0 > 0) {
-      float up[4], uh = 0.0f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) up[c] = 0.0f;
-      if (J0 > 0) load_row<VEC>(x, g, I0 - 1, J0 - 1, K0, up, uh);
-      float d1up[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) d1up[c] = up[c] - (c ? up[c - 1] : uh);
-#pragma unroll
-      for (int r = 0; r < RW; ++r) {
-        float v[4], h;
-        load_row<VEC>(x, g, I0 - 1, J0 + r, K0, v, h);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float d1 = v[c] - (c ? v[c - 1] : h);
-          dprev[r][c] = d1 - d1up[c];
-          d1up[c] = d1;
-        }
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < PL; ++p) {
-      const int64_t i = I0 + p;
-      float d1up[4];
-      {
-        float up[4], uh = 0.0f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) up[c] = 0.0f;
-        if (D >= 2 && J0 > 0) load_row<VEC>(x, g, i, J0 - 1, K0, up, uh);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) d1up[c] = up[c] - (c ? up[c - 1] : uh);
-      }
-#pragma unroll
-      for (int r = 0; r < RW; ++r) {
-        const int64_t j = J0 + r;
-        float v[4], h;
-        load_row<VEC>(x, g, i, j, K0, v, h);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          blk[(p * RW + r) * 4 + c] = v[c];
-          const float d1 = v[c] - (c ? v[c - 1] : h);
-          const float d2 = d1 - d1up[c];
-          d1up[c] = d1;
-          const float d = d2 - dprev[r][c];
-          dprev[r][c] = d2;
-          const int64_t k = K0 + c;
-          const bool real = (i < g.n[0]) && (j < g.n[1]) && (k < g.n[2]);
-          const bool origin = (i == 0) && (j == 0) && (k == 0);
-          sz_put<DBG>(d, r_f, real && !origin, sh_hist, ws.hist, ovf,
-                      DBG ? dbg.codes + (i * g.n[1] + j) * g.n[2] + k : nullptr);
-        }
-      }
-    }
     uint32_t bits;
     double E;
-    int emax;
-    int cf[SZ];
-    uint32_t u[SZ];
-    zfp_block<D, DBG>(blk, minexp, bits, E, emax, cf, u);
+    block_estimate<D, VEC, DBG>(x, g, t, r_f, minexp, sh_hist, ws.hist, ovf, dbg, bits, E);
     bits_acc += bits;
     err_acc += E;
-    if constexpr (DBG) {
-      dbg.emax[t] = emax;
-      dbg.bits[t] = bits;
-      dbg.err[t] = E;
-#pragma unroll
-      for (int n = 0; n < SZ; ++n) {
-        dbg.coef[t * SZ + n] = cf[n];
-        dbg.uword[t * SZ + n] = u[n];
-      }
-    }
   }
   // per-CTA partial in a fixed order (deterministic): warp tree, then warps in order
 #pragma unroll
@@ -683,6 +694,290 @@ int launch_finalize(const Workspace &ws, const FinalizeArgs &fa, sel_result *d_o
   return launch_pdl((const void *)k_finalize, dim3(kFinCTAs), dim3(kFinThreads), 0, st, args) ==
                  cudaSuccess
              ? SEL_OK : SEL_ECUDA;
+}
+
+// ============================================================ small single field
+// k_small: one launch estimates one small field (N <= 2^21): value range -> per-block SZ
+// + ZFP -> entropy / result, separated by two grid-wide barriers on a co-resident grid
+// (cooperative launch) instead of three launches or k_batch's cross-CTA task hand-offs
+// (k_batch: ~44 us for one 256x256 field).  The last CTA resets the
+// barrier counters, the range keys and (as every CTA does for its slice) the histogram,
+// so the next call starts from the same state; results are bit-identical to the per-field
+// kernels (same per-block code, fixed-order partial sums).
+struct SmallState {
+  unsigned int rmin, rmax, rbad, ctr, ticket, pad[3];
+};
+struct SmallFin { double acc; unsigned long long hcnt, ovf; };
+#ifndef SEL_SMALL_PROF
+#define SEL_SMALL_PROF 0               // developer probe: %globaltimer at k_small's phase ends (CTA 0)
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned int sk_key(float v) {   // order-preserving float key
+  const unsigned int b = __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float sk_float(unsigned int k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+__device__ __forceinline__ void grid_barrier(unsigned int *ctr, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    long long guard = 0;
+    while (ld_acquire(ctr) < target) {
+      __nanosleep(32);
+      if (++guard > (1LL << 26)) __trap();
+    }
+  }
+  __syncthreads();
+}
+
+template <int D, bool VEC>
+__global__ void __launch_bounds__(256) k_small(const float *__restrict__ x, Geo g, SmallState *st,
+                                               unsigned long long *gh, Partial *part, SmallFin *fin,
+                                               Params *prm_out, FinalizeArgs fa, sel_result *out) {
+  extern __shared__ unsigned int sh_hist[];
+  const unsigned long long T0 = SEL_SMALL_PROF ? gtimer() : 0ull;
+  __shared__ float s_mn[8], s_mx[8];
+  __shared__ int s_bad[8];
+  __shared__ bool s_last;
+  hist_zero(sh_hist);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // ---- phase 1: value range (Alg. 1 line 2, R1); NaN-propagating min, +-inf in min / max
+  {
+    float mn = INFINITY, mx = -INFINITY;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    auto take = [&](float v) {
+      mn = (v != v || v < mn) ? v : mn;
+      mx = fmaxf(mx, v);
+    };
+    if (VEC) {   // float4 loads, 4 in flight per thread (one L2 round trip for C1)
+      const float4 *x4 = reinterpret_cast<const float4 *>(x);
+      const int64_t n4 = g.N / 4;
+      for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += 4 * gs) {
+        float4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = i0 + u * gs;
+          q[u] = i < n4 ? __ldg(x4 + i) : make_float4(x[0], x[0], x[0], x[0]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { take(q[u].x); take(q[u].y); take(q[u].z); take(q[u].w); }
+      }
+    } else {
+      for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < g.N; i0 += 4 * gs) {
+        float q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = i0 + u * gs;
+          q[u] = i < g.N ? __ldg(x + i) : x[0];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) take(q[u]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float a = __shfl_xor_sync(0xffffffffu, mn, o);
+      mn = (a != a || a < mn) ? a : mn;
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nw; ++w) {
+        mn = (s_mn[w] != s_mn[w] || s_mn[w] < mn) ? s_mn[w] : mn;
+        mx = fmaxf(mx, s_mx[w]);
+      }
+      const int bad = (mn != mn) | ((mn <= mx) & (is_nonfinite(mn) | is_nonfinite(mx)));
+      if (mn <= mx) {
+        atomicMin(&st->rmin, sk_key(mn));
+        atomicMax(&st->rmax, sk_key(mx));
+      }
+      if (bad) atomicOr(&st->rbad, 1u);
+    }
+  }
+  const unsigned long long T1 = SEL_SMALL_PROF ? gtimer() : 0ull;
+  grid_barrier(&st->ctr, gridDim.x);
+  const unsigned long long T2 = SEL_SMALL_PROF ? gtimer() : 0ull;
+  const Params prm = make_params(sk_float(__ldcg(&st->rmin)), sk_float(__ldcg(&st->rmax)), (int)__ldcg(&st->rbad),
+                                 fa.mode, fa.eb);
+  // ---- phase 2: every processed block (R3-R14), per-CTA partial in a fixed order
+  uint64_t bits_acc = 0;
+  double err_acc = 0.0;
+  unsigned int ovf = 0;
+  if (prm.status == SEL_OK) {
+    const DebugPtrs nd{};
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < g.n_pb; t += gs) {
+      uint32_t bits;
+      double E;
+      block_estimate<D, VEC, false>(x, g, t, prm.r_f, prm.minexp, sh_hist, gh, ovf, nd, bits, E);
+      bits_acc += bits;
+      err_acc += E;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bits_acc += __shfl_down_sync(0xffffffffu, bits_acc, o);
+    err_acc += __shfl_down_sync(0xffffffffu, err_acc, o);
+  }
+  __shared__ uint64_t sb[8];
+  __shared__ double se[8];
+  if (lane == 0) { sb[wid] = bits_acc; se[wid] = err_acc; }
+  ovf_flush(ovf, gh);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w) { bits_acc += sb[w]; err_acc += se[w]; }
+    Partial pr;
+    pr.bits = bits_acc;
+    pr.err = err_acc;
+    part[blockIdx.x] = pr;
+  }
+  const unsigned long long T3 = SEL_SMALL_PROF ? gtimer() : 0ull;
+  hist_flush(sh_hist, gh);
+  const unsigned long long T4 = SEL_SMALL_PROF ? gtimer() : 0ull;
+  grid_barrier(&st->ctr, 2 * gridDim.x);
+  const unsigned long long T5 = SEL_SMALL_PROF ? gtimer() : 0ull;
+  if (SEL_SMALL_PROF && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long *pr = (unsigned long long *)(fin + gridDim.x);
+    pr[0] = T1 - T0; pr[1] = T2 - T1; pr[2] = T3 - T2; pr[3] = T4 - T3; pr[4] = T5 - T4;
+  }
+  // ---- phase 3: this CTA's slice of the histogram: sum c log2(N/c), re-zero (R6)
+  {
+    const int per = (kNSlots + gridDim.x - 1) / gridDim.x;
+    const int s0 = blockIdx.x * per, s1 = min(s0 + per, kNSlots);
+    const double lN = log2((double)fa.n_sz);
+    double acc = 0.0;
+    unsigned long long hcnt = 0, novf = 0;
+    for (int sl = s0 + threadIdx.x; sl < s1; sl += blockDim.x) {
+      const unsigned long long c = __ldcg(gh + sl);
+      hcnt += c;
+      if (c) {
+        const double cd = (double)c;
+        acc += cd * (lN - log2(cd));
+        gh[sl] = 0ull;
+      }
+      if (sl == kOvfSlot) novf = c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc += __shfl_down_sync(0xffffffffu, acc, o);
+      hcnt += __shfl_down_sync(0xffffffffu, hcnt, o);
+      novf += __shfl_down_sync(0xffffffffu, novf, o);
+    }
+    __shared__ double sa[8];
+    __shared__ unsigned long long sh[8], so[8];
+    if (lane == 0) { sa[wid] = acc; sh[wid] = hcnt; so[wid] = novf; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nw; ++w) { acc += sa[w]; hcnt += sh[w]; novf += so[w]; }
+      SmallFin f;
+      f.acc = acc;
+      f.hcnt = hcnt;
+      f.ovf = novf;
+      fin[blockIdx.x] = f;
+      __threadfence();
+      s_last = atomicAdd(&st->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+  }
+  if (!s_last || wid != 0) return;
+  // ---- the last CTA, warp 0: fixed-order sums (lane-strided loads, one shuffle tree),
+  // the result (Eq. entropy, psnr-sz, ZFP, Alg. 1 lines 7-10), and the reset
+  __threadfence();
+  double S = 0.0, errs = 0.0;
+  unsigned long long tb = 0, hc = 0, ov = 0;
+  for (unsigned int c = lane; c < gridDim.x; c += 32) {
+    S += __ldcg(&fin[c].acc);
+    hc += __ldcg(&fin[c].hcnt);
+    ov += __ldcg(&fin[c].ovf);
+    tb += __ldcg(&part[c].bits);
+    errs += __ldcg(&part[c].err);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    S += __shfl_down_sync(0xffffffffu, S, o);
+    errs += __shfl_down_sync(0xffffffffu, errs, o);
+    tb += __shfl_down_sync(0xffffffffu, tb, o);
+    hc += __shfl_down_sync(0xffffffffu, hc, o);
+    ov += __shfl_down_sync(0xffffffffu, ov, o);
+  }
+  // the three logarithms of the result on three lanes at once (as k_finalize does)
+  const double mse = __shfl_sync(0xffffffffu, errs, 0) / (double)fa.n_values;
+  const bool okp = prm.status == SEL_OK;
+  double lg = 0.0;
+  if (lane == 1 && okp) lg = log10(prm.vr / prm.eb_abs);
+  if (lane == 2 && okp) lg = log10(prm.vr);
+  if (lane == 3 && mse > 0.0) lg = log10(mse);
+  const double lg_vr_eb = __shfl_sync(0xffffffffu, lg, 1), lg_vr = __shfl_sync(0xffffffffu, lg, 2),
+               lg_mse = __shfl_sync(0xffffffffu, lg, 3);
+  if (lane != 0) return;
+  if (SEL_SMALL_PROF) {
+    unsigned long long *pr = (unsigned long long *)(fin + gridDim.x);
+    pr[5] = gtimer() - T5;   // phase 3 + the last CTA (the last CTA's own T5)
+    pr[6] = blockIdx.x;
+  }
+  *prm_out = prm;
+  *out = assemble_result(prm, S, errs, tb, ov, hc, fa, lg_vr_eb, lg_vr, lg_mse);
+  st->rmin = 0xffffffffu;
+  st->rmax = 0u;
+  st->rbad = 0u;
+  st->ctr = 0u;
+  st->ticket = 0u;
+}
+
+namespace {
+template <int D, bool VEC>
+const void *small_fn() { return (const void *)k_small<D, VEC>; }
+const void *pick_small(int D, bool vec) {
+  if (D == 1) return vec ? small_fn<1, true>() : small_fn<1, false>();
+  if (D == 2) return vec ? small_fn<2, true>() : small_fn<2, false>();
+  return vec ? small_fn<3, true>() : small_fn<3, false>();
+}
+}  // namespace
+
+size_t small_state_bytes(int sm_count) {
+  return 256 + (size_t)sm_count * (sizeof(Partial) + sizeof(SmallFin)) + 512;
+}
+
+// one-time init of the small-field state (range keys at their neutral values)
+int init_small_state(void *state, cudaStream_t st) {
+  SmallState s{};
+  s.rmin = 0xffffffffu;
+  return cudaMemcpyAsync(state, &s, sizeof(s), cudaMemcpyHostToDevice, st) == cudaSuccess ? SEL_OK : SEL_ECUDA;
+}
+
+int launch_small(const float *x, const Geo &g, int sm_count, void *state, const Workspace &ws,
+                 const FinalizeArgs &fa, sel_result *d_out, cudaStream_t st) {
+  const void *fn = pick_small(g.ndims, g.vec != 0);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, kEstSmem) != cudaSuccess || occ < 1)
+    return SEL_ECUDA;
+  const int64_t ctas = sm_count;                         // one CTA per SM: co-resident
+  SmallState *ss = (SmallState *)state;
+  Partial *part = (Partial *)((char *)state + 256);
+  SmallFin *fin = (SmallFin *)(part + sm_count);
+  Geo gg = g;
+  FinalizeArgs f = fa;
+  unsigned long long *gh = ws.hist;
+  Params *prm = ws.params;
+  void *args[] = {(void *)&x, (void *)&gg, (void *)&ss, (void *)&gh, (void *)&part, (void *)&fin,
+                  (void *)&prm, (void *)&f, (void *)&d_out};
+#ifndef SEL_SMALL_PLAIN
+#define SEL_SMALL_PLAIN 0              // developer probe: plain (non-cooperative) launch
+#endif
+  if (SEL_SMALL_PLAIN)
+    return cudaLaunchKernel(fn, dim3((unsigned)ctas), dim3(256), args, kEstSmem, st) == cudaSuccess ? SEL_OK : SEL_ECUDA;
+  return cudaLaunchCooperativeKernel(fn, dim3((unsigned)ctas), dim3(256), args, kEstSmem, st) == cudaSuccess
+             ? SEL_OK
+             : SEL_ECUDA;
 }
 
 }  // namespace sel

@@ -791,3 +791,45 @@ def test_zfp_stream_errors(sel):
         with pytest.raises(sel.SelError) as e:
             p.compress_zfp(torch.ones(8, 8, device="cuda"))
         assert e.value.status == sel.SEL_EDEGENERATE
+
+
+# ---------------------------------------------------------------- small single fields
+@pytest.mark.parametrize("shape,stride", [((256, 256), None), ((203, 517), None), ((100003,), None),
+                                          ((37, 45, 70), None), ((64, 64, 64), (4, 4, 4)), ((120, 400), (1, 10)),
+                                          ((5,), None), ((1, 1, 8), None), ((1024, 1024), None)])
+def test_small_kernel_vs_oracle_and_batch(sel, orc, shape, stride):
+    """One small field through sel_estimate runs the single cooperative launch k_small
+    (value range -> blocks -> entropy / result); it equals the oracle and the k_batch /
+    per-field path (1e-12), repeats bit-identically, and is one launch."""
+    rng = np.random.default_rng(sum(shape))
+    x = np.cumsum(rng.standard_normal(shape), axis=-1).astype(np.float32)
+    t = torch.from_numpy(x).cuda()
+    with sel.Plan(shape, 1e-4, "rel", stride) as p:
+        l0 = p.launch_count
+        a = p.estimate(t)
+        assert p.launch_count - l0 == 1
+        b = p.estimate(t)
+        p.set_option("small_kernel", 0)
+        c = p.estimate(t)
+    assert a == b
+    compare_scalars(a, orc.estimate(x, 1e-4, stride=stride), f"small{shape}")
+    for k in a:
+        if isinstance(a[k], float):
+            assert close(a[k], c[k], rel=1e-12), (k, a[k], c[k])
+        else:
+            assert a[k] == c[k], k
+
+
+def test_small_kernel_status(sel):
+    with sel.Plan((16, 16), 1e-3) as p:
+        with pytest.raises(sel.SelError) as e:
+            p.estimate(torch.ones(16, 16, device="cuda"))
+        assert e.value.status == sel.SEL_EDEGENERATE
+        for bad in (float("nan"), float("inf"), -float("inf")):
+            y = torch.arange(256, dtype=torch.float32, device="cuda").view(16, 16).clone()
+            y[5, 7] = bad
+            with pytest.raises(sel.SelError) as e:
+                p.estimate(y)
+            assert e.value.status == sel.SEL_ENONFINITE
+        ok = p.estimate(torch.arange(256, dtype=torch.float32, device="cuda").view(16, 16))   # state was reset
+        assert ok["status"] == 0
