@@ -114,6 +114,7 @@ struct sel_plan_st {
   // small-field single-launch state (first use)
   void *small_mem = nullptr;
   int use_small = 1;              // option "small_kernel"
+  int range_warps = 1;            // option "range_warps": k_batch<3> streams the value range on its own warps
   // N3 ZFP stream workspace (first use): per-block lengths, CTA bases, total
   void *zs_mem = nullptr;
   // N2 paper-literal workspace (first use): CTA partials, mid scalars, params, result
@@ -312,7 +313,7 @@ int enqueue_batch(sel_plan_t p, const float *const *x, int n, cudaStream_t st,
     }
   }
   int rc = launch_batch(g, p->tl[0], p->bs, x, n, p->bstate, p->bstate_cap, fa, p->mode, p->eb,
-                        d_res ? d_res : p->d_res, p->sm_count, G, p->lag_t, &p->btab, dump, st,
+                        d_res ? d_res : p->d_res, p->sm_count, G, p->lag_t, p->range_warps, &p->btab, dump, st,
                         p->timing ? p->bev : nullptr);
   if (rc == SEL_ECUDA) return cuda_fail(cudaGetLastError(), "k_batch launch");
   if (rc) return rc;
@@ -662,6 +663,10 @@ int sel_set_option(sel_plan_t p, const char *key, double value) {
   }
   if (!strcmp(key, "batch_debug")) {
     p->batch_debug = value != 0.0;
+    return SEL_OK;
+  }
+  if (!strcmp(key, "range_warps")) {
+    p->range_warps = value != 0.0;
     return SEL_OK;
   }
   if (!strcmp(key, "small_kernel")) {

@@ -85,6 +85,9 @@ struct BatchArgs {
   int nR, nT, phase;              // tasks per field (F: kFinTasks); phase = kFinTasks + nR + nT
   const uint4 *ttab;              // decoded task sequences of all groups (host-built)
   int rchunk;                     // floats per R task
+  int rw;                         // 1: the value range is streamed by the range warps (no R tasks)
+  int nRc, rcf;                   // range-warp chunks per field, floats per chunk
+  unsigned int *rtask_ctr;        // [G] range-warp chunk counter of each group
   FinalizeArgs fa;
   int mode;
   double eb;
@@ -219,8 +222,18 @@ enum { REQ_T = 1, REQ_R = 2, REQ_END = 3 };
 struct RelReq { int kind, f; unsigned int cnt, rmin, rmax, rbad; };
 constexpr int kRelQ = 16;
 
+// Range warps (3D): extra warps that stream the value range of the fields ahead of the
+// tiles straight from global memory into registers (LDG.128, 32 in flight per lane), so the
+// stage ring carries tiles only and a tile loads while the previous one is computed (with R
+// tasks interleaved on a 2-stage ring every tile load waited for the tile before it).
+#ifndef SEL_RW3
+#define SEL_RW3 2
+#endif
 template <int D>
-constexpr int batch_threads() { return (TileCfg<D>::CW + 2) * 32; }   // + producer + release warp
+constexpr int range_warps() { return D == 3 ? SEL_RW3 : 0; }
+template <int D>
+constexpr int batch_threads() { return (TileCfg<D>::CW + 2 + range_warps<D>()) * 32; }   // + producer + release warp
+constexpr int kRwChunk = 16384;                // floats per range-warp chunk (64 KB)
 
 // producer: wait until a stage is free.  SEL_PWAIT = 0: probe + nanosleep back-off;
 // otherwise a hardware-suspended mbarrier.try_wait with that time hint (ns): the thread
@@ -246,6 +259,21 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity
   }
 }
 
+// Named barriers for the waits inside the CTA.  A warp blocked in bar.sync issues nothing;
+// an mbarrier try_wait / nanosleep poll does not stay asleep while bulk copies land in the
+// CTA (every complete_tx wakes NANOSLEEP.SYNCS: ncu showed the producer's stage wait looping
+// every ~8 ns, ~10 % of the kernel's issued instructions, and the release warp's queue poll
+// another ~5 %).  Ids: 0 __syncthreads, 1 consumers, 2 + s "stage s is free" (consumer
+// warps arrive, the producer warp syncs), kBarReq the consumer warp 0 <-> release warp
+// hand-over (both sync: a rendezvous per request).
+constexpr int kBarStage = 2, kBarReq = 8;
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // warp 0 lane 0 spins until *flag >= target (acquire); the caller syncs the consumers
 __device__ __forceinline__ void spin_until(const unsigned int *flag, unsigned int target) {
   unsigned int ns = 32;
@@ -255,6 +283,53 @@ __device__ __forceinline__ void spin_until(const unsigned int *flag, unsigned in
     if (ns < 1024) ns <<= 1;
     if (++guard > (1LL << 24)) __trap();     // never hang the GPU on a logic error
   }
+}
+
+
+// ---- value range by streaming warps (rw mode): chunk c of a group = (local field c / nRc,
+// chunk c % nRc), claimed in order from the group's counter by the range warps and by
+// consumer warps that are waiting for a field's parameters.
+__device__ __forceinline__ float4 ldg_keep(const float4 *p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+struct RangeAcc { float mn, mx, mn2, mx2; unsigned int cnt; };
+__device__ __forceinline__ void range_reset(RangeAcc &r) {
+  r.mn = r.mn2 = INFINITY;
+  r.mx = r.mx2 = -INFINITY;
+  r.cnt = 0u;
+}
+// min / max of one chunk (n4 float4, 16-byte aligned) into the warp's accumulators; NaN
+// propagates through min.NaN (R1), 32 loads in flight per lane
+__device__ __forceinline__ void range_chunk(const float4 *__restrict__ src, int n4, int lane,
+                                            uint64_t pol, RangeAcc &r) {
+  constexpr int U = 32;
+  int i = lane;
+#pragma unroll 1
+  for (; i + (U - 1) * 32 < n4; i += U * 32) {
+    float4 q[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) q[k] = ldg_keep(src + i + k * 32, pol);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      r.mn = fmin3_nan(r.mn, q[k].x, q[k].y);
+      r.mx = fmax3(r.mx, q[k].x, q[k].y);
+      r.mn2 = fmin3_nan(r.mn2, q[k].z, q[k].w);
+      r.mx2 = fmax3(r.mx2, q[k].z, q[k].w);
+    }
+  }
+#pragma unroll 1
+  for (; i < n4; i += 32) {
+    const float4 q = ldg_keep(src + i, pol);
+    r.mn = fmin3_nan(r.mn, q.x, q.y);
+    r.mx = fmax3(r.mx, q.x, q.y);
+    r.mn2 = fmin3_nan(r.mn2, q.z, q.w);
+    r.mx2 = fmax3(r.mx2, q.z, q.w);
+  }
+  ++r.cnt;
 }
 
 template <int D>
@@ -280,7 +355,6 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   __shared__ int s_chunk[NCHUNK];                // window chunks with a nonzero bin (flush)
   __shared__ unsigned int s_rmin[2], s_rmax[2], s_rbad[2], s_rcnt[2];
   __shared__ RelReq s_q[kRelQ];
-  __shared__ unsigned int s_qhead, s_qtail;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int grp = (int)(blockIdx.x % (unsigned)a.G);
@@ -289,23 +363,66 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   // this group's task table: groups before it hold (fields with f % G < grp) sequences
   const uint4 *const ttab = a.ttab + (long long)a.phase * ((long long)grp * (a.nf / a.G) + min(grp, a.nf % a.G));
   if (tid == 0) {
-    s_qhead = 0u;
-    s_qtail = 0u;
     for (int k = 0; k < 2; ++k) {
       s_rmin[k] = 0xffffffffu; s_rmax[k] = 0u; s_rbad[k] = 0u; s_rcnt[k] = 0u;
     }
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], CW);
     }
     fence_barrier_init();
   }
   for (int i = tid; i < Cfg::HIST_WORDS; i += (int)blockDim.x) hist[i] = 0u;
   __syncthreads();
 
+  // ---- rw mode: chunk claim / publish (range warps, and consumer warps waiting for params)
+  const bool rw_on = range_warps<D>() > 0 && a.rw != 0;     // (compiled out of the 2D kernel)
+  const unsigned int rw_total = rw_on ? (unsigned)nfl * (unsigned)a.nRc : 0u;
+  auto rw_claim = [&]() -> unsigned int {
+    unsigned int c = 0u;
+    if (lane == 0) c = atomicAdd(a.rtask_ctr + grp, 1u);
+    return __shfl_sync(0xffffffffu, c, 0);
+  };
+  // the warp's accumulated chunks of local field l -> the field's global min / max keys;
+  // the last contributor of the field writes params(f) (Alg. 1 line 2)
+  auto rw_publish = [&](int l, RangeAcc &r) {
+    if (r.cnt) {
+      float mn = fmin_nan(r.mn, r.mn2), mx = fmaxf(r.mx, r.mx2);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin_nan(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (lane == 0) {
+        const int g = l * a.G + grp;
+        const int bad = (mn != mn) | ((mn <= mx) & (is_nonfinite(mn) | is_nonfinite(mx)));
+        if (mn <= mx) {
+          atomicMin(a.rmin + g, float_key(mn));
+          atomicMax(a.rmax + g, float_key(mx));
+        }
+        if (bad) atomicOr(a.rbad + g, 1u);
+        fence_acq_rel_gpu();
+        if (atomicAdd(a.rdone + g, r.cnt) + r.cnt == (unsigned)a.nRc) {   // last
+          fence_acq_rel_gpu();
+          const float fmn = key_float(ld_acquire(a.rmin + g)), fmx = key_float(ld_acquire(a.rmax + g));
+          a.params[g] = make_params(fmn, fmx, (int)ld_acquire(a.rbad + g), a.mode, a.eb);
+          fence_acq_rel_gpu();
+          st_release(a.params_ready + g, 1u);
+        }
+      }
+      __syncwarp();
+    }
+    range_reset(r);
+  };
+  auto rw_chunk = [&](unsigned int c, uint64_t pol, RangeAcc &r) {   // chunk c of this group
+    const int l = (int)(c / (unsigned)a.nRc), i = (int)(c % (unsigned)a.nRc);
+    const long long lo = (long long)i * a.rcf;
+    const int n4 = (int)(min((long long)a.rcf, a.N - lo) >> 2);
+    range_chunk(reinterpret_cast<const float4 *>(a.xs[l * a.G + grp] + lo), n4, lane, pol, r);
+  };
+
   // ------------------------------------------------------------------ producer
   if (warp == CW) {
-    if (lane == 0) {
+    {
       int stage = 0;
       uint32_t ph = 0;
       // L2 policies: a range task's chunk is read again by the field's tiles two phases
@@ -352,8 +469,11 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       // one batch ahead: the claim's round trip to L2 (a counter shared by the group's
       // CTAs) is off the producer's critical path (it was ~2,000 cycles per task).
       constexpr unsigned int K = SEL_CLAIM;
-      long long cb = (long long)atomicAdd(a.task_ctr + grp, K);
-      long long nb = cb < ntot ? (long long)atomicAdd(a.task_ctr + grp, K) : ntot;
+      long long cb = ntot, nb = ntot;
+      if (lane == 0) {
+        cb = (long long)atomicAdd(a.task_ctr + grp, K);
+        nb = cb < ntot ? (long long)atomicAdd(a.task_ctr + grp, K) : ntot;
+      }
       unsigned int ck = 0;
       auto next_tau = [&]() -> long long {
         if (ck == K) {
@@ -365,17 +485,28 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         return t < ntot ? t : ntot;
       };
       Dec t0, t1;
-      long long tau_n = next_tau();
-      decode_pf(tau_n, fetch(tau_n), t0);
-      tau_n = next_tau();
-      decode_pf(tau_n, fetch(tau_n), t1);
-      tau_n = t1.kind < 0 ? ntot : next_tau();
-      uint4 e_n = fetch(tau_n);          // in flight: the task after t1
+      t0.kind = t1.kind = -1;
+      long long tau_n = ntot;
+      uint4 e_n = make_uint4(0u, 0u, 0u, 0u);
+      if (lane == 0) {
+        tau_n = next_tau();
+        decode_pf(tau_n, fetch(tau_n), t0);
+        tau_n = next_tau();
+        decode_pf(tau_n, fetch(tau_n), t1);
+        tau_n = t1.kind < 0 ? ntot : next_tau();
+        e_n = fetch(tau_n);              // in flight: the task after t1
+      }
+      __syncwarp();
       long long pp_start = PCLOCK(), pp_wait = 0, pp_dec = 0, pp_n = 0;
+      long long posted = 0;
+      // every lane walks the loop (the stage wait is a warp-level bar.sync); lane 0 works
       for (;;) {
         const long long pw0 = PCLOCK();
-        mbar_wait_backoff(&empty_bar[stage], ph ^ 1u);
+        if (posted >= Cfg::STAGES) bar_sync_n(kBarStage + stage, (CW + 1) * 32);
+        ++posted;
         PROF(pp_wait += clock64() - pw0; ++pp_n);
+        int done = 0;
+        if (lane == 0) {
         stage_desc[stage] = make_int4(t0.kind, t0.f, t0.id, t0.phase);
         stage_tile[stage] = make_int4(t0.btk, t0.btj, t0.bi, t0.slot);
         float *dst = base + stage * Cfg::STAGE_FLOATS;
@@ -395,17 +526,23 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         } else {
           mbar_arrive(&full_bar[stage]);   // F / sampled T / sentinel: no staged data
         }
+        done = t0.kind < 0;
+        }
+        done = __shfl_sync(0xffffffffu, done, 0);
         if (++stage == Cfg::STAGES) { stage = 0; ph ^= 1u; }
-        if (t0.kind < 0) break;            // the sentinel went out: done
+        if (done) break;                   // the sentinel went out: done
+        if (lane == 0) {
         t0 = t1;
         const long long pd0 = PCLOCK();
         decode_pf(tau_n, e_n, t1);
         tau_n = t1.kind < 0 ? ntot : next_tau();
         e_n = fetch(tau_n);
         PROF(pp_dec += clock64() - pd0);
+        }
+        __syncwarp();
       }
 #if SEL_BATCH_PROF
-      if (a.prof) {
+      if (a.prof && lane == 0) {
         atomicAdd(a.prof + 148 * 8 + 8, (unsigned long long)(clock64() - pp_start));
         atomicAdd(a.prof + 148 * 8 + 9, (unsigned long long)pp_wait);
         atomicAdd(a.prof + 148 * 8 + 10, (unsigned long long)pp_dec);
@@ -418,18 +555,13 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
 
   // ------------------------------------------------------------------ release warp
   if (warp == CW + 1) {
-    if (lane == 0) {
-      unsigned int t = 0;
-      unsigned int ns = SEL_RSLEEP;
-      for (;;) {
-        if (t == ld_acquire_cta(&s_qhead)) {
-          __nanosleep(ns);
-          if (ns < 2048) ns <<= 1;        // requests are rare; polling steals issue slots
-          continue;
-        }
-        ns = SEL_RSLEEP;
-        const RelReq r = s_q[t % kRelQ];
-        if (r.kind == REQ_END) break;
+    // one rendezvous (bar.sync kBarReq) per request: consumer warp 0 wrote s_q[t % kRelQ]
+    // before it; blocked in the barrier the warp issues nothing
+    for (unsigned int t = 0;; ++t) {
+      bar_sync_n(kBarReq, 64);
+      const RelReq r = s_q[t % kRelQ];
+      if (r.kind == REQ_END) break;
+      if (lane == 0) {
         if (r.kind == REQ_T) {
           fence_acq_rel_gpu();
           atomicAdd(a.tdone + r.f, r.cnt);
@@ -447,9 +579,34 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
             st_release(a.params_ready + g, 1u);
           }
         }
-        ++t;
-        st_release_cta(&s_qtail, t);
       }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ range warps
+  if (warp >= CW + 2) {
+    if (rw_on) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      RangeAcc r;
+      range_reset(r);
+      int curl = -1;
+      unsigned int c = rw_claim();
+      while (c < rw_total) {
+        const unsigned int cn = rw_claim();     // the next claim's round trip overlaps this chunk
+        const int l = (int)(c / (unsigned)a.nRc);
+        if (l != curl) {
+          if (curl >= 0) rw_publish(curl, r);   // nothing is held across the wait below
+          curl = l;
+          // (no pacing against the tiles: a wait here would be a poll loop, and polls steal
+          // issue slots from the consumer warps; the range simply runs ahead of the tiles)
+        }
+        rw_chunk(c, pol, r);
+        c = cn;
+      }
+      if (curl >= 0) rw_publish(curl, r);
     }
     return;
   }
@@ -468,16 +625,18 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // wait, flush, T, R, F, release, #flush, #publish
 #endif
 
-  unsigned int qh = 0;             // tid 0: next request slot
+  unsigned int qh = 0;             // consumer warp 0: next request slot
   auto enqueue = [&](int kind, int f, unsigned int cnt, unsigned int rmn, unsigned int rmx,
-                     unsigned int rbd) {   // tid 0 only
+                     unsigned int rbd) {   // every lane of consumer warp 0
     const long long tp0 = PCLOCK();
-    while (qh - ld_acquire_cta(&s_qtail) >= (unsigned)kRelQ) __nanosleep(32);
-    RelReq r;
-    r.kind = kind; r.f = f; r.cnt = cnt; r.rmin = rmn; r.rmax = rmx; r.rbad = rbd;
-    s_q[qh % kRelQ] = r;
+    if (lane == 0) {
+      RelReq r;
+      r.kind = kind; r.f = f; r.cnt = cnt; r.rmin = rmn; r.rmax = rmx; r.rbad = rbd;
+      s_q[qh % kRelQ] = r;
+    }
     ++qh;
-    st_release_cta(&s_qhead, qh);
+    __syncwarp();
+    bar_sync_n(kBarReq, 64);        // hand-over: the release warp reads the slot after it
     PROF(pc[5] += clock64() - tp0);
   };
 
@@ -499,7 +658,6 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     const long long q1 = PCLOCK();
     consumer_sync<NC>();
     const long long q2 = PCLOCK();
-    PROF(pc[6] += 1);
     for (int c = warp; c < NCHUNK; c += CW) {
       const uint4 *h4 = reinterpret_cast<const uint4 *>(hist + c * kChunk);
       uint32_t any = 0u;
@@ -543,7 +701,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       atomicAdd(a.prof + 148 * 8 + 2, (unsigned long long)(q3 - q2));
       atomicAdd(a.prof + 148 * 8 + 3, (unsigned long long)(q4 - q3));
     }
-    if (tid == 0) enqueue(REQ_T, cur, cur_tasks, 0u, 0u, 0u);
+    if (warp == 0) enqueue(REQ_T, cur, cur_tasks, 0u, 0u, 0u);
     cur = -1;
     cur_tasks = 0;
   };
@@ -556,18 +714,21 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
   int cur_phase = 0;
   auto leave_phase = [&]() {
     consumer_sync<NC>();
-    if (tid == 0) {
+    if (warp == 0) {
       const int pp = cur_phase & 1;
-      const unsigned int cnt = s_rcnt[pp];
+      const unsigned int cnt = s_rcnt[pp], rmn = s_rmin[pp], rmx = s_rmax[pp], rbd = s_rbad[pp];
+      __syncwarp();
+      if (lane == 0) {
+        s_rmin[pp] = 0xffffffffu;
+        s_rmax[pp] = 0u;
+        s_rbad[pp] = 0u;
+        s_rcnt[pp] = 0u;
+      }
       if (cnt) {
         const int g = cur_phase * a.G + grp;                      // R(p) belongs to local field p
-        enqueue(REQ_R, g, cnt, s_rmin[pp], s_rmax[pp], s_rbad[pp]);
+        enqueue(REQ_R, g, cnt, rmn, rmx, rbd);
         PROF(pc[7] += 1);
       }
-      s_rmin[pp] = 0xffffffffu;
-      s_rmax[pp] = 0u;
-      s_rbad[pp] = 0u;
-      s_rcnt[pp] = 0u;
     }
   };
 
@@ -597,7 +758,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     const long long t_k0 = PCLOCK();
     PROF(pc[1] += t_k0 - t_w1);      // publish + flush
     if (end) {
-      if (tid == 0) enqueue(REQ_END, 0, 0u, 0u, 0u, 0u);
+      if (warp == 0) enqueue(REQ_END, 0, 0u, 0u, 0u, 0u);
       break;
     }
     const float *S = base + stage * Cfg::STAGE_FLOATS;
@@ -607,7 +768,27 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       if (cur < 0) {               // first tile of field f here: params, ring slot free
         // per warp (no CTA barrier): lane 0 acquires the flags, the warp barrier orders
         // the lanes' L2 reads (ld.cg: never a stale L1 line) after it
-        if (lane == 0) {
+        if (rw_on) {               // help with the value range while waiting for params(f)
+          uint64_t pol;
+          asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+          RangeAcc r;
+          range_reset(r);
+          bool more = true;
+          for (;;) {
+            unsigned int rdy = 0u;
+            if (lane == 0) rdy = ld_acquire(a.params_ready + f);
+            if (__shfl_sync(0xffffffffu, rdy, 0)) break;
+            const unsigned int c = more ? rw_claim() : rw_total;
+            if (c < rw_total) {
+              rw_chunk(c, pol, r);
+              rw_publish((int)(c / (unsigned)a.nRc), r);      // at once: nothing held while waiting
+            } else {
+              more = false;
+              __nanosleep(256);
+            }
+          }
+          if (lane == 0 && f >= kRing * a.G) spin_until(a.fin_ready + f - kRing * a.G, 1u);
+        } else if (lane == 0) {
           spin_until(a.params_ready + f, 1u);
           if (f >= kRing * a.G) spin_until(a.fin_ready + f - kRing * a.G, 1u);   // slot's last user
         }
@@ -626,13 +807,15 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
                            a.hist + (size_t)tc.w * kH32Stride + 1, ovf, tbits,
                            terr);
       } else {
+        PROF(const long long tq0 = clock64());
         tile_consume<D, false>(S, tc.x, tc.y, tc.z, a.tg, warp, lane, ok, r_f, minexp, hist,
                                a.hist + (size_t)tc.w * kH32Stride + 1, ovf,
                                nodbg, tbits, terr);
+        PROF(pc[6] += clock64() - tq0);   // the tile compute alone
       }
       ++cur_tasks;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      bar_arrive_n(kBarStage + stage, (CW + 1) * 32);
       task_store(a.tpart + (size_t)tc.w * a.nT * CW, id * CW + warp, tbits, terr);
     } else if (kind == KIND_R) {
       // ---- min / max / non-finite of the staged chunk (R1) by kRWarps consumer warps
@@ -641,7 +824,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       const int slot = (warp - (id * kRWarps) % CW + CW) % CW;
       if (slot >= kRWarps) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[stage]);
+        bar_arrive_n(kBarStage + stage, (CW + 1) * 32);
       } else {
         const long long lo = (long long)id * a.rchunk;
         const int n4 = (int)min((long long)a.rchunk, a.N - lo) / 4;
@@ -661,7 +844,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
         mn = fmin_nan(mn, mn2);
         mx = fmaxf(mx, mx2);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[stage]);
+        bar_arrive_n(kBarStage + stage, (CW + 1) * 32);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           mn = fmin_nan(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -682,7 +865,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
     } else if (kind == KIND_F) {
       const int slot = stage_tile[stage].w;   // read before the stage is released
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      bar_arrive_n(kBarStage + stage, (CW + 1) * 32);
       if (tid == 0) spin_until(a.tdone + f, (unsigned)a.nT);
       consumer_sync<NC>();
       unsigned int *gh = a.hist + (size_t)slot * kH32Stride + 1;
@@ -768,7 +951,7 @@ __global__ void __launch_bounds__(batch_threads<D>(), 1) k_batch(const BatchArgs
       }
     } else {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      bar_arrive_n(kBarStage + stage, (CW + 1) * 32);
     }
 #if SEL_BATCH_PROF
     {
@@ -827,7 +1010,7 @@ int batch_ntasks(const Geo &g, const TileLaunch &tl, const BatchSizes &bs) {
 
 size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G) {
   return (size_t)nf * (sizeof(Params) + 8 * 4 + sizeof(CUtensorMap) + 8) + 64 +
-         (size_t)G * kRing * ((size_t)kH32Stride * 4 + (size_t)nT * bs.cw * sizeof(Partial) +
+         (size_t)G * 8 + (size_t)G * kRing * ((size_t)kH32Stride * 4 + (size_t)nT * bs.cw * sizeof(Partial) +
                               kFinTasks * sizeof(FPart)) +
          8192;
 }
@@ -861,7 +1044,7 @@ static void build_group_sequence(int nfl, int nR, int nT, int lagT, int lagF, co
 
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
-                 sel_result *d_results, int sm_count, int G, int lagT, BatchTable *tab,
+                 sel_result *d_results, int sm_count, int G, int lagT, int range_warps_on, BatchTable *tab,
                  const BatchDump &dump, cudaStream_t st, cudaEvent_t *ev) {
   if (!tab || !batch_fits(g, tl, bs, nf)) return SEL_EINVAL;
   if (G < 1 || G > nf || G > sm_count || lagT < 1 || lagT > 4) return SEL_EINVAL;
@@ -876,13 +1059,16 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   };
   const int nT = batch_ntasks(g, tl, bs);
   const bool sampled = g.s[0] > 1 || g.s[1] > 1 || g.s[2] > 1;
+  // range warps (3D full-field stacks): no R tasks in the sequence
+  const bool rw = range_warps_on && !sampled && g.ndims == 3 && range_warps<3>() > 0;
+  const int nRs = rw ? 0 : bs.nR;
   // the histogram ring first, at a fixed offset: its slots stay zero between launches
   const size_t nslot = (size_t)G * kRing;
   unsigned int *hst = (unsigned int *)take((size_t)kH32Stride * 4 * nslot);
   CUtensorMap *tmaps = (CUtensorMap *)take(sizeof(CUtensorMap) * nf, 128);
   const float **xs = (const float **)take(sizeof(float *) * nf);
   Params *params = (Params *)take(sizeof(Params) * nf);
-  const size_t nctr = 8 * (size_t)nf + (size_t)G;
+  const size_t nctr = 8 * (size_t)nf + 2 * (size_t)G;
   unsigned int *ctrs = (unsigned int *)take(sizeof(unsigned int) * nctr);
   Partial *tp = (Partial *)take(sizeof(Partial) * (size_t)nT * bs.cw * nslot);
   FPart *fp = (FPart *)take(sizeof(FPart) * kFinTasks * nslot);
@@ -916,18 +1102,21 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   a.g = g;
   a.sampled = sampled ? 1 : 0;
   a.N = g.N;
-  a.nR = bs.nR;
+  a.nR = nRs;
   a.nT = nT;
-  a.phase = kFinTasks + bs.nR + nT;
+  a.phase = kFinTasks + nRs + nT;
+  a.rw = rw ? 1 : 0;
+  a.rcf = kRwChunk;
+  a.nRc = (int)((g.N + kRwChunk - 1) / kRwChunk);
   if ((long long)nf * a.phase >= (1LL << 31)) return SEL_EINVAL;   // 32-bit task indices
   {   // task table, rebuilt only when its key changes
-    const long long key[8] = {nf, G, bs.nR, nT, lagT, sampled ? 1 : 0, tl.tg.ntk, tl.tg.ntj};
+    const long long key[8] = {nf, G, nRs, nT, lagT, sampled ? 1 : 0, tl.tg.ntk, tl.tg.ntj};
     if (memcmp(key, tab->key, sizeof(key)) != 0) {
       static thread_local std::vector<uint4> h;
       h.clear();
       h.reserve((size_t)nf * a.phase);
       for (int gi = 0; gi < G; ++gi)
-        build_group_sequence((nf - gi + G - 1) / G, bs.nR, nT, lagT, lagT + 2, tl.tg, sampled, h);
+        build_group_sequence((nf - gi + G - 1) / G, nRs, nT, lagT, lagT + 2, tl.tg, sampled, h);
       const size_t bytes = h.size() * sizeof(uint4);
       if (bytes > tab->cap) {
         if (tab->d) { cudaStreamSynchronize(st); cudaFree(tab->d); }
@@ -955,6 +1144,7 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   a.rmin = ctrs + 6 * nf;
   a.rbad = ctrs + 7 * nf;
   a.task_ctr = ctrs + 8 * nf;
+  a.rtask_ctr = ctrs + 8 * nf + G;
   a.G = G;
   a.lagT = lagT;
   a.lagF = lagT + 2;

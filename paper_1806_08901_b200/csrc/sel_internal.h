@@ -157,7 +157,7 @@ size_t batch_state_bytes(int nf, const BatchSizes &bs, int nT, int G);
 int batch_ntasks(const Geo &g, const TileLaunch &tl, const BatchSizes &bs);
 int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const float *const *d_fields,
                  int nf, void *state, size_t state_bytes, const FinalizeArgs &fa, int mode, double eb,
-                 sel_result *d_results, int sm_count, int G, int lagT, BatchTable *tab,
+                 sel_result *d_results, int sm_count, int G, int lagT, int range_warps_on, BatchTable *tab,
                  const BatchDump &dump, cudaStream_t st, cudaEvent_t *ev);
 int plan_tile(const Geo &g, int sm_count, int debug, TileLaunch *tl);
 int launch_tile(const float *x, const Geo &g, const TileLaunch &tl, const Workspace &ws,

@@ -186,7 +186,9 @@ __device__ __forceinline__ float lane_rf(bool act, float r_f) {   // NaN: every 
 // Consumer work of one tile task (block-layer bi, tile row btj, tile column btk; warp-level:
 // every consumer warp of the CTA calls it for the same tile).  S: the tile's smem stage.  Adds the SZ codes to the CTA's histogram
 // (lane copies / packed table / ghist / ovf) and returns the lane's block bits/error.
-template <int D, bool DBG, typename GH = unsigned long long>
+// ROLE: 0 = SZ then ZFP by the same warp; 1 = the SZ half only, 2 = the ZFP half only (the
+// two halves read the tile independently, so they can run on different warps).
+template <int D, bool DBG, typename GH = unsigned long long, int ROLE = 0>
 __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, int bi,
                                              const TileGeo &tg, int warp,
                                              int lane, bool ok, float r_f, int minexp,
@@ -213,6 +215,9 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
       const float *wrow = S + (4 * wr) * kBoxK;     // smem row of j = J0 - 1 (plane 0)
       const float rf = lane_rf(activeK, r_f);
       // ---------------- SZ: nested differences on the tile (R4), codes -> histogram (R5)
+      static_assert(D == 3 || ROLE == 0, "split roles: 3D only");
+      float blk2[D == 2 ? 16 : 1];   // 2D: the ZFP block is rows 1..4 of the SZ plane
+      if constexpr (ROLE != 2) {
       float dprev[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -235,7 +240,6 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
       // Blocks away from the far edges and the field origin (warp-uniform) skip the per-row
       // bound / origin checks and the edge replication.
       const bool edge = J0 + 4 > n1 || (D == 3 && I0 + 4 > n0) || (btk == 0 && J0 == 0 && I0 == 0);
-      float blk2[D == 2 ? 16 : 1];   // 2D: the ZFP block is rows 1..4 of the SZ plane
       auto rows = [&](auto EDGE, int i, const float (&v)[5][4], const float (&h)[5], float (&d1up)[4]) {
         constexpr bool E = decltype(EDGE)::value;
 #pragma unroll
@@ -295,8 +299,9 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
         if (edge) rows(std::true_type{}, i, v, h, d1up);
         else rows(std::false_type{}, i, v, h, d1up);
       }
+      }
       // ---------------- ZFP on the lane's block, edge-replicated at the far edges (R17)
-      if (activeK) {
+      if (ROLE != 1 && activeK) {
         float blk[SZ];
         if constexpr (D == 2) {
 #pragma unroll

@@ -15,6 +15,9 @@ PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
 def run(fields, eb, stride, label):
     shape = tuple(fields[0].shape)
     p = sel.Plan(shape, eb, "rel", stride)
+    for kv in os.environ.get("SEL_OPTS", "").split(","):      # e.g. SEL_OPTS=range_warps=0,groups=2
+        if kv:
+            p.set_option(kv.split("=")[0], float(kv.split("=")[1]))
     buf = p.results_buffer(len(fields))
     for _ in range(2):
         p.estimate_batch_async(fields, buf)
