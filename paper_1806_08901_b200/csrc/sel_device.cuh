@@ -188,9 +188,16 @@ __device__ __forceinline__ bool zfp_transform(const float (&v)[Tab<D>::SIZE], in
 #pragma unroll
     for (int n = 0; n < SZ; ++n) cf[n] = __float2int_rz(__fmul_rn(v[n], sc));
   } else {
+    // (rare: blocks below 2^-97.  The empty volatile asm keeps this a real branch -- without
+    // it the compiler evaluates both scalings for every block and selects: 3 FMUL + 1 FSEL
+    // per value instead of 1 FMUL.)
     const float sc = __uint_as_float((uint32_t)(93 - emax) << 23);
 #pragma unroll
-    for (int n = 0; n < SZ; ++n) cf[n] = __float2int_rz(__fmul_rn(__fmul_rn(v[n], 0x1p64f), sc));
+    for (int n = 0; n < SZ; ++n) {
+      float t = __fmul_rn(v[n], 0x1p64f);
+      asm volatile("" : "+f"(t));
+      cf[n] = __float2int_rz(__fmul_rn(t, sc));
+    }
   }
   // decorrelating lift along the fastest axis first, then slower (R8)
 #pragma unroll
@@ -255,7 +262,9 @@ __device__ __forceinline__ void zfp_cost(const int (&cf)[Tab<D>::SIZE], int emax
     constexpr int j = SZ - 1 - decltype(JJ)::value;
     constexpr int n = Tab<D>::make_perm().v[j];
     constexpr int c = Tab<D>::cls_of(n);
-    const uint32_t uj = to_negabinary(cf[n]);
+    // negabinary u = (c + M) ^ M; its dropped digits (u & low) ^ (M & low) = (c + M) & low
+    const uint32_t tj = (uint32_t)cf[n] + 0xAAAAAAAAu;
+    const uint32_t uj = tj ^ 0xAAAAAAAAu;
     if constexpr (DBG) u[j] = uj;
     const int f = flo(uj);
     if constexpr (j == SZ - 1) fL = f;
@@ -265,7 +274,7 @@ __device__ __forceinline__ void zfp_cost(const int (&cf)[Tab<D>::SIZE], int emax
     }
     R = max(R, f);
     sR += R;
-    const int e = (int)((uj & low) ^ Mk) - (int)Mk;
+    const int e = (int)(tj & low) - (int)Mk;
     acc[c] += (unsigned long long)((long long)e * (long long)e);
   });
   if (prec == 0) {

@@ -134,17 +134,13 @@ __device__ __forceinline__ void consumer_sync() {   // the consumer threads only
 // column, which TMA zero-filled at the field's left edge).  All loads are issued first.
 __device__ __forceinline__ void load_plane(const float *prow, int lane, float (&v)[5][4],
                                            float (&h)[5]) {
-  float h0[5];
+  // the left neighbour straight from the tile (a 16-byte lane stride: 4 wavefronts, but one
+  // instruction instead of a broadcast load + shuffle + select; the LSU has the headroom)
 #pragma unroll
   for (int r = 0; r < 5; ++r) {
     const float4 q = *reinterpret_cast<const float4 *>(prow + r * kBoxK + 4 + 4 * lane);
     v[r][0] = q.x; v[r][1] = q.y; v[r][2] = q.z; v[r][3] = q.w;
-    h0[r] = prow[r * kBoxK + 3];
-  }
-#pragma unroll
-  for (int r = 0; r < 5; ++r) {
-    const float hs = __shfl_up_sync(0xffffffffu, v[r][3], 1);
-    h[r] = lane == 0 ? h0[r] : hs;
+    h[r] = prow[r * kBoxK + 3 + 4 * lane];
   }
 }
 
@@ -307,17 +303,27 @@ __device__ __forceinline__ void tile_consume(const float *S, int btk, int btj, i
 #pragma unroll
           for (int n = 0; n < 16; ++n) blk[n] = blk2[n];
         } else {
+          const float *bbase = S + Cfg::PLANE + (4 * wr + 1) * kBoxK + 4 + 4 * lane;
+          if (J0 + 4 <= n1 && I0 + 4 <= n0) {        // interior (warp-uniform): fixed offsets
 #pragma unroll
-          for (int p = 0; p < NPL; ++p) {
-            const int ic = min(I0 + p, n0 - 1) - I0;          // 0..3, edge-replicated
-            const float *pbase = S + (ic + 1) * Cfg::PLANE;
+            for (int p = 0; p < NPL; ++p)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int jc = min(J0 + r, n1 - 1) - J0;         // 0..3
-              const float4 q = *reinterpret_cast<const float4 *>(
-                  pbase + (4 * wr + 1 + jc) * kBoxK + 4 + 4 * lane);
-              const int o = (p * 4 + r) * 4;
-              blk[o] = q.x; blk[o + 1] = q.y; blk[o + 2] = q.z; blk[o + 3] = q.w;
+              for (int r = 0; r < 4; ++r) {
+                const float4 q = *reinterpret_cast<const float4 *>(bbase + p * Cfg::PLANE + r * kBoxK);
+                const int o = (p * 4 + r) * 4;
+                blk[o] = q.x; blk[o + 1] = q.y; blk[o + 2] = q.z; blk[o + 3] = q.w;
+              }
+          } else {
+#pragma unroll
+            for (int p = 0; p < NPL; ++p) {
+              const int ic = min(I0 + p, n0 - 1) - I0;          // 0..3, edge-replicated
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                const int jc = min(J0 + r, n1 - 1) - J0;         // 0..3
+                const float4 q = *reinterpret_cast<const float4 *>(bbase + ic * Cfg::PLANE + jc * kBoxK);
+                const int o = (p * 4 + r) * 4;
+                blk[o] = q.x; blk[o + 1] = q.y; blk[o + 2] = q.z; blk[o + 3] = q.w;
+              }
             }
           }
         }
