@@ -88,6 +88,21 @@ class PaperResult(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class VariantResult(C.Structure):
+    """Mirror of orc_variant_result (orc.h): the variant quantisers, SURVEY 8(f) N4."""
+    _fields_ = [
+        ("lin_bits", C.c_double), ("lin_psnr", C.c_double),
+        ("log_bits", C.c_double), ("log_psnr", C.c_double), ("log_mse", C.c_double),
+        ("eqp_bits", C.c_double), ("eqp_psnr", C.c_double), ("eqp_mse", C.c_double),
+        ("eqp_width_sum", C.c_double), ("value_range", C.c_double), ("eb_abs", C.c_double),
+        ("n_in", C.c_uint64), ("hist_ovf", C.c_uint64),
+        ("log_base", C.c_int32), ("log_bins", C.c_int32), ("eqp_n", C.c_int32), ("status", C.c_int32),
+    ]
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class Debug(C.Structure):
     _fields_ = [("codes", C.c_void_p), ("hist", C.c_void_p), ("emax", C.c_void_p),
                 ("coef", C.c_void_p), ("uword", C.c_void_p), ("bits", C.c_void_p),
@@ -108,6 +123,10 @@ def lib():
             L.orc_estimate_mt.restype = C.c_int
             L.orc_estimate_paper.argtypes = [P, C.c_int, P, C.c_int, C.c_double, P, C.c_double, P]
             L.orc_estimate_paper.restype = C.c_int
+            L.orc_variants_from_hist.argtypes = [P, C.c_double, C.c_double, C.c_int, C.c_int, P]
+            L.orc_variants_from_hist.restype = C.c_int
+            L.orc_estimate_variants.argtypes = [P, C.c_int, P, C.c_int, C.c_double, P, C.c_int, C.c_int, P]
+            L.orc_estimate_variants.restype = C.c_int
             L.orc_paper_positions.argtypes = [C.c_int, P]
             L.orc_paper_positions.restype = C.c_int
             L.orc_block_paper.argtypes = [P, C.c_int, C.c_int, C.c_int32, P, P]
@@ -243,6 +262,34 @@ def estimate_paper(x: np.ndarray, eb: float, mode: str = "rel", stride=None,
                                    None if st is None else _ptr(st), float(sz_offset), C.byref(res))
     if st_ != 0:
         raise OracleError(st_)
+    return res.to_dict()
+
+
+def variants_from_hist(hist: np.ndarray, value_range: float, eb_abs: float, log_base: int = 2,
+                       eqp_n: int = 128) -> dict:
+    """SURVEY 8(f) N4 on a given 65,536-slot code histogram (orc_variants_from_hist)."""
+    h = np.ascontiguousarray(hist, dtype=np.uint64)
+    assert h.size == NSLOTS
+    res = VariantResult()
+    rc = lib().orc_variants_from_hist(_ptr(h), float(value_range), float(eb_abs), int(log_base), int(eqp_n),
+                                      C.byref(res))
+    if rc != 0:
+        raise OracleError(rc)
+    return res.to_dict()
+
+
+def estimate_variants(x: np.ndarray, eb: float, mode: str = "rel", stride=None, log_base: int = 2,
+                      eqp_n: int = 128) -> dict:
+    """SURVEY 8(f) N4 (orc_estimate_variants): the log-scale and equal-probability
+     quantisation estimates, with the linear one by the same general equations
+    (P:396-403), on the field's code histogram (the stored PDF)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    nd, dims, st = _dims_stride(x.shape, stride)
+    res = VariantResult()
+    rc = lib().orc_estimate_variants(_ptr(x), nd, _ptr(dims), 1 if mode == "rel" else 0, float(eb),
+                                     None if st is None else _ptr(st), int(log_base), int(eqp_n), C.byref(res))
+    if rc != 0:
+        raise OracleError(rc)
     return res.to_dict()
 
 

@@ -982,3 +982,124 @@ int orc_zfp_stream_decode(const uint8_t *buf, uint64_t nbits, int nd, const int6
   }
   return pos == nbits ? ORC_OK : ORC_EINVAL;
 }
+
+/* ------------------------------------------------------------------ */
+/* log-scale and equal-probability quantisation         */
+/* estimates on the stored PDF; see orc.h.          */
+/* ------------------------------------------------------------------ */
+int orc_variants_from_hist(const uint64_t *hist, double VR, double eb_abs, int b, int n,
+                           orc_variant_result *out) {
+  if (!hist || !out || b < 2 || n < 1 || n > 32768) return ORC_EINVAL;
+  memset(out, 0, sizeof(*out));
+  out->value_range = VR;
+  out->eb_abs = eb_abs;
+  out->log_base = b;
+  out->eqp_n = n;
+  out->hist_ovf = hist[ORC_OVF_SLOT];
+  const int C0 = 32767;                         /* slot of code 0 */
+  uint64_t N = 0;
+  for (int s = 0; s < ORC_OVF_SLOT; ++s) N += hist[s];
+  out->n_in = N;
+  if (N == 0) { out->status = ORC_EDEGENERATE; return ORC_EDEGENERATE; }
+  const double delta = 2.0 * eb_abs;
+  /* linear: bins = cells */
+  {
+    double H = 0.0;
+    for (int s = 0; s < ORC_OVF_SLOT; ++s) {
+      if (!hist[s]) continue;
+      const double p = (double)hist[s] / (double)N;
+      H -= p * log2(p);
+    }
+    out->lin_bits = H;
+    out->lin_psnr = 20.0 * log10(VR / delta) + 10.0 * log10(12.0);   /* Eq. psnr-pdf-linear */
+  }
+  /* log-scale: bin index i = floor(log_b |q|) by repeated multiplication */
+  {
+    uint64_t cnt[2][17];
+    double width[17];
+    memset(cnt, 0, sizeof cnt);
+    uint64_t central = 0;
+    for (int s = 0; s < ORC_OVF_SLOT; ++s) {
+      if (!hist[s]) continue;
+      const int q = s - C0;
+      const int64_t a = q < 0 ? -(int64_t)q : q;
+      if (a < b) { central += hist[s]; continue; }
+      int i = 0;
+      int64_t pw = b;                            /* b^(i+1) */
+      while (pw * b <= a) { pw *= b; ++i; }
+      /* now b^(i+1) <= a < b^(i+2): bin i + 1 */
+      cnt[q < 0][i + 1] += hist[s];
+    }
+    {
+      double pw = 1.0;                           /* width of bin i >= 1: b^(i+1) - b^i cells */
+      for (int i = 1; i < 17; ++i) { pw *= (double)b; width[i] = pw * (double)b - pw; }
+    }
+    double H = 0.0, M = 0.0;
+    int used = 0;
+    if (central) {
+      const double p = (double)central / (double)N, w = (double)(2 * b - 1) * delta;
+      H -= p * log2(p);
+      M += w * w * p;
+      ++used;
+    }
+    for (int sg = 0; sg < 2; ++sg)
+      for (int i = 1; i < 17; ++i) {
+        if (!cnt[sg][i]) continue;
+        const double p = (double)cnt[sg][i] / (double)N, w = width[i] * delta;
+        H -= p * log2(p);
+        M += w * w * p;
+        ++used;
+      }
+    out->log_bits = H;
+    out->log_mse = M / 12.0;
+    out->log_psnr = 20.0 * log10(VR) - 10.0 * log10(out->log_mse);
+    out->log_bins = used;
+  }
+  /* equal-probability: edges s_k = F^-1(k / (2n-1)) in cell units */
+  {
+    const uint64_t K = (uint64_t)(2 * n - 1);
+    int lo = 0, hi = ORC_OVF_SLOT - 1;
+    while (!hist[lo]) ++lo;
+    while (!hist[hi]) --hi;
+    double prev = (double)(lo - C0) - 0.5;        /* s_0 */
+    double sum2 = 0.0, sumw = 0.0;
+    uint64_t cum = 0;                             /* mass below cell s */
+    int s = lo;
+    for (uint64_t k = 1; k <= K; ++k) {
+      double edge;
+      if (k == K) {
+        edge = (double)(hi - C0) + 0.5;           /* s_(2n-1) */
+      } else {
+        const uint64_t T = k * N;                 /* target mass x K */
+        while ((cum + hist[s]) * K <= T) { cum += hist[s]; ++s; }   /* cum K <= T < (cum + c_s) K */
+        const double frac = (double)(T - cum * K) / ((double)hist[s] * (double)K);
+        edge = ((double)(s - C0) - 0.5) + frac;
+      }
+      const double w = edge - prev;
+      sum2 += w * w;
+      sumw += w;
+      prev = edge;
+    }
+    out->eqp_width_sum = sumw;
+    out->eqp_bits = 1.0 + log2((double)n);
+    out->eqp_mse = delta * delta * sum2 / (12.0 * (double)K);
+    out->eqp_psnr = 20.0 * log10(VR) - 10.0 * log10(out->eqp_mse);
+  }
+  out->status = ORC_OK;
+  return ORC_OK;
+}
+
+int orc_estimate_variants(const float *x, int ndims, const int64_t *dims, int eb_mode, double eb,
+                          const int32_t *stride, int log_base, int eqp_n, orc_variant_result *out) {
+  if (!out) return ORC_EINVAL;
+  uint64_t *hist = (uint64_t *)calloc(ORC_NSLOTS, sizeof(uint64_t));
+  if (!hist) return ORC_EINVAL;
+  orc_result r;
+  orc_debug dbg;
+  memset(&dbg, 0, sizeof dbg);
+  dbg.hist = hist;
+  int rc = orc_estimate(x, ndims, dims, eb_mode, eb, stride, 0.5, &r, &dbg);
+  if (rc == ORC_OK) rc = orc_variants_from_hist(hist, r.value_range, r.eb_abs, log_base, eqp_n, out);
+  free(hist);
+  return rc;
+}

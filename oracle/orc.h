@@ -122,6 +122,39 @@ int orc_zfp_stream(const float *x, int ndims, const int64_t *dims, int eb_mode, 
 int orc_zfp_stream_decode(const uint8_t *buf, uint64_t nbits, int ndims, const int64_t *dims, int eb_mode,
                           double eb, double value_range, const int32_t *stride, float *out);
 
+/* ---- the variant quantisers of Section 5.1.4 evaluated with
+ * the general Stage-II estimators -- BR = -sum_i P_i log2 P_i (Eq. bit-rate-pdf),
+ * MSE = (1/12) sum_i delta_i^2 P_i (delta_i^3 P(m_i) = delta_i^2 P_i), PSNR =
+ * 20 log10 VR - 10 log10 MSE (Eq. psnr-pdf) -- on the approximate PDF the
+ * selector stores: the n_pdf = 65,535-bin code histogram, cell q = [(q - 1/2)
+ * delta, (q + 1/2) delta), delta = 2 eb_abs, mass c_q / N_in, uniform inside a cell
+ * (reading R21; codes in the overflow slot lie outside the PDF's support).
+ *  linear: the bins are the cells; BR = the entropy of the in-range codes,
+ *    PSNR = Eq. psnr-pdf-linear.
+ *  log-scale, integer base b >= 2: bin(q) = n + sign(q) floor(log_b |q|), the
+ *    central bin n holds |q| < b (width 2b - 1 cells; printed delta_n = 2b on the
+ *    continuum), bin n +- i holds b^i <= |q| < b^(i+1) (width b^(i+1) - b^i cells).
+ *  equal-probability, 2n - 1 bins: edges at the quantiles k / (2n - 1) of the
+ *    piecewise-linear CDF, s_0 / s_(2n-1) = the outer edges of the lowest / highest
+ *    occupied cell; BR = 1 + log2 n as printed, MSE from the general equation with
+ *    P_i = 1 / (2n - 1) (no K-means: P:428 calls it expensive, SURVEY A21 rules it out). */
+typedef struct {
+  double lin_bits, lin_psnr;
+  double log_bits, log_psnr, log_mse;
+  double eqp_bits, eqp_psnr, eqp_mse;
+  double eqp_width_sum;        /* sum_k delta_k in cells = (highest - lowest occupied cell) + 1 */
+  double value_range, eb_abs;
+  uint64_t n_in;               /* in-range codes (the PDF's mass)                             */
+  uint64_t hist_ovf;
+  int32_t log_base, log_bins;  /* occupied log-scale bins                                     */
+  int32_t eqp_n;
+  int32_t status;
+} orc_variant_result;
+int orc_variants_from_hist(const uint64_t *hist, double value_range, double eb_abs, int log_base,
+                           int eqp_n, orc_variant_result *out);
+int orc_estimate_variants(const float *x, int ndims, const int64_t *dims, int eb_mode, double eb,
+                          const int32_t *stride, int log_base, int eqp_n, orc_variant_result *out);
+
 /* ---- single steps, exported for the pin tests ---- */
 float orc_lorenzo(const float *x, int ndims, const int64_t *dims, const int64_t *idx);
 int32_t orc_quantize(float d, float r_f);

@@ -815,3 +815,127 @@ def test_zfp_stream_empty_and_constant(orc):
     assert nbits == r["zfp_total_bits"]
     y = orc.zfp_stream_decode(buf, nbits, c.shape, 1e-3, r["value_range"], mode="abs")
     assert np.abs(y - c).max() <= 1e-3
+
+
+# ---------------------------------------------------------------- N4: variant quantisers
+def _hist_of(codes):
+    h = np.zeros(65536, np.uint64)
+    for q, c in codes.items():
+        h[32767 + int(q)] = c
+    return h
+
+
+def test_variants_hand_example(orc):
+    """SURVEY 8(f) N4, reading R21: the log-scale and equal-probability
+     quantisers evaluated with Eq. bit-rate-pdf and MSE = (1/12)
+    sum delta_i^2 P_i on a 4-cell PDF, against values worked by hand
+    (tests/golden/variants_hand.json)."""
+    g = gold("variants_hand.json")
+    r = orc.variants_from_hist(_hist_of(g["hist"]), g["value_range"], g["eb_abs"], g["log_base"], g["eqp_n"])
+    delta = 2 * g["eb_abs"]
+    H = -sum(p * math.log2(p) for p in g["log_bins_P"])
+    assert r["log_bits"] == pytest.approx(H, rel=1e-14) and r["log_bins"] == 2
+    assert r["log_mse"] == pytest.approx(g["log_mse_times_12"] * delta ** 2 / 12, rel=1e-14)
+    assert 12 * r["log_mse"] == pytest.approx(
+        sum(p * (w * delta) ** 2 for p, w in zip(g["log_bins_P"], g["log_bin_widths_cells"])), rel=1e-14)
+    e = g["eqp_edges_cells"]
+    assert r["eqp_mse"] == pytest.approx(sum((b - a) ** 2 for a, b in zip(e, e[1:])) * delta ** 2 / 36, rel=1e-14)
+    assert r["eqp_mse"] == pytest.approx(g["eqp_mse_times_36"] / 36, rel=1e-14)
+    assert r["eqp_bits"] == g["eqp_bits"] and r["lin_bits"] == g["lin_bits"]
+    assert r["eqp_width_sum"] == pytest.approx(4.0, rel=1e-14)
+    for k in ("log", "eqp"):
+        assert r[k + "_psnr"] == pytest.approx(20 * math.log10(g["value_range"]) - 10 * math.log10(r[k + "_mse"]), rel=1e-14)
+
+
+def test_variants_closed_forms(orc):
+    """Closed forms the equations fix: (i) a base above every |code| leaves one log bin:
+    BR = 0 and MSE = ((2b-1) delta)^2 / 12; (ii) equal counts in 2n-1 adjacent cells: the
+    equal-probability bins ARE the cells, so its MSE and PSNR are the linear quantiser's
+    delta^2 / 12 and Eq. psnr-pdf-linear, and BR = 1 + log2 n; (iii) all the
+    mass in one cell: 2n-1 equal slices of width delta / (2n-1); (iv) the linear BR is the
+    Shannon entropy of the counts and its PSNR equals Eq. psnr-sz."""
+    eb, vr = 0.25, 100.0
+    delta = 2 * eb
+    h = _hist_of({-5: 7, 0: 100, 3: 9, 11: 1})
+    r = orc.variants_from_hist(h, vr, eb, 12, 3)
+    assert r["log_bits"] == 0.0 and r["log_bins"] == 1
+    assert r["log_mse"] == pytest.approx((23 * delta) ** 2 / 12, rel=1e-14)
+    assert r["lin_bits"] == pytest.approx(-sum(c / 117 * math.log2(c / 117) for c in (7, 100, 9, 1)), rel=1e-14)
+    assert r["lin_psnr"] == pytest.approx(-20 * math.log10(eb / vr) + 10 * math.log10(3), rel=1e-13)
+    for n in (1, 2, 5, 64):
+        m = n - 1
+        u = _hist_of({q: 13 for q in range(-m, m + 1)})
+        r = orc.variants_from_hist(u, vr, eb, 2, n)
+        assert r["eqp_mse"] == pytest.approx(delta ** 2 / 12, rel=1e-13)
+        assert r["eqp_psnr"] == pytest.approx(r["lin_psnr"], rel=1e-13)
+        assert r["eqp_bits"] == pytest.approx(1 + math.log2(n), rel=1e-15)
+        one = _hist_of({4: 1000})
+        r = orc.variants_from_hist(one, vr, eb, 2, n)
+        assert r["eqp_mse"] == pytest.approx((delta / (2 * n - 1)) ** 2 / 12, rel=1e-12)
+        assert r["eqp_width_sum"] == pytest.approx(1.0, rel=1e-12)
+
+
+def test_variants_brute_force_from_residuals(orc):
+    """Brute force through the whole estimate: the log-scale bins by math.log per code and the
+    equal-probability edges as quantiles of the sorted codes, from the field's own codes
+    (independent of the oracle's histogram walk); merging cells can only lower the entropy
+    and raise the MSE (BR_log <= BR_lin, MSE_log >= delta^2 / 12); the widths tile the
+    occupied support."""
+    rng = np.random.default_rng(7)
+    g = np.cumsum(np.cumsum(rng.standard_normal((48, 60)), 0), 1).astype(np.float32)
+    for eb, b, n in ((1e-3, 2, 16), (1e-4, 3, 128), (3e-3, 10, 7)):
+        full = orc.estimate(g, eb, debug=True)
+        codes = full["debug"]["codes"].ravel()
+        q = codes[(codes >= 0) & (codes < 65535)].astype(np.int64) - 32767
+        r = orc.estimate_variants(g, eb, log_base=b, eqp_n=n)
+        assert r["n_in"] == q.size and r["hist_ovf"] == int((codes == 65535).sum())
+        delta = 2 * full["eb_abs"]
+        # log-scale: bin id per code
+        ids = []
+        for v in q:
+            a = abs(int(v))
+            if a < b:
+                ids.append(0)
+                continue
+            i = int(math.floor(math.log(a, b) + 1e-12))
+            while b ** i > a:
+                i -= 1
+            while b ** (i + 1) <= a:
+                i += 1
+            ids.append(i if v > 0 else -i)
+        ids = np.array(ids)
+        H = M = 0.0
+        for i in np.unique(ids):
+            p = float((ids == i).mean())
+            w = (2 * b - 1) if i == 0 else (b ** (abs(i) + 1) - b ** abs(i))
+            H -= p * math.log2(p)
+            M += p * (w * delta) ** 2 / 12
+        assert r["log_bits"] == pytest.approx(H, rel=1e-10)
+        assert r["log_mse"] == pytest.approx(M, rel=1e-10)
+        assert r["log_bits"] <= r["lin_bits"] + 1e-12 and r["log_mse"] >= delta ** 2 / 12 * (1 - 1e-12)
+        # equal-probability: the quantiles from the SORTED codes (no histogram): the unit of
+        # mass number floor(k N / K) sits in cell qs[floor(k N / K)], at the fraction of that
+        # cell's samples below it
+        qs = np.sort(q)
+        N, K = qs.size, 2 * n - 1
+        s = [qs[0] - 0.5]
+        for k in range(1, K):
+            m = Fraction(k * N, K)
+            cell = int(qs[int(m)])
+            below = int(np.searchsorted(qs, cell, side="left"))
+            inside = int(np.searchsorted(qs, cell, side="right")) - below
+            s.append(cell - 0.5 + float((m - below) / inside))
+        s.append(qs[-1] + 0.5)
+        mse = float(((np.diff(np.array(s, dtype=np.float64)) * delta) ** 2).sum() / (12 * K))
+        assert r["eqp_width_sum"] == pytest.approx(float(qs[-1] - qs[0] + 1), rel=1e-12)
+        assert r["eqp_mse"] == pytest.approx(mse, rel=1e-10)
+        assert r["eqp_bits"] == 1 + math.log2(n)
+
+
+def test_variants_invalid_arguments(orc):
+    h = _hist_of({0: 1})
+    for b, n in ((1, 4), (2, 0), (2, 40000)):
+        with pytest.raises(Exception):
+            orc.variants_from_hist(h, 1.0, 0.1, b, n)
+    with pytest.raises(Exception):
+        orc.variants_from_hist(np.zeros(65536, np.uint64), 1.0, 0.1, 2, 4)   # no mass
