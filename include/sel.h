@@ -114,6 +114,28 @@ typedef struct {
   int32_t status;
 } sel_paper_result;
 
+/* the variant quantisers of the paper's Section 5.1.4 evaluated with its
+ * general Stage-II estimators -- BR = -sum_i P_i log2 P_i (Eq. bit-rate-pdf), MSE
+ * = (1/12) sum_i delta_i^2 P_i, PSNR = 20 log10 VR - 10 log10 MSE (Eq. psnr-pdf,
+ * P:377-380) -- on the PDF the selector stores, the field's 65,535-bin code histogram
+ * (P:637): cell q = [(q - 1/2) delta, (q + 1/2) delta), delta = 2 eb_abs, uniform inside
+ * (reading R21; codes in the overflow slot are outside the PDF). */
+typedef struct {
+  double lin_bits, lin_psnr; /* linear: entropy of the in-range codes, Eq. psnr-pdf-linear */
+  double log_bits, log_psnr; /* log-scale, integer base b: central bin |q| < b, bin +-i  */
+  double log_mse;            /* holds b^i <= |q| < b^(i+1) (widths 2b - 1 and b^(i+1) - b^i cells)   */
+  double eqp_bits, eqp_psnr; /* equal-probability, 2n - 1 bins: BR = 1 + log2 n,  */
+  double eqp_mse;            /* edges at the quantiles k / (2n - 1) of the piecewise-linear CDF,      */
+                             /* MSE = delta^2 sum_k w_k^2 / (12 (2n - 1))                             */
+  double eqp_width_sum;      /* sum_k w_k (cells) = occupied support                                  */
+  double value_range, eb_abs;
+  uint64_t n_in;             /* in-range codes (the PDF's mass)                                       */
+  uint64_t hist_ovf;         /* codes in the overflow slot                                            */
+  int32_t log_base, log_bins;/* b; occupied log-scale bins                                            */
+  int32_t eqp_n;             /* n                                                                     */
+  int32_t status;
+} sel_variant_result;
+
 /* Create a plan for fields of shape dims[0..ndims-1].
  *   mode, eb : SEL_EB_ABS -> eb_abs = eb; SEL_EB_REL -> eb_abs = eb * VR (Alg.1 line 2)
  *   stride   : ndims entries >= 1, block b is processed iff b_a % stride[a] == 0 for
@@ -121,7 +143,7 @@ typedef struct {
  *   block    : ZFP block edge, must be 4
  * Allocates the device workspace on the current device.  Errors: SEL_EINVAL,
  * SEL_ENOMEM, SEL_ECUDA. */
-int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double eb,
+int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, sel_eb_mode mode, double eb,
              const int32_t *stride, int32_t block);
 
 /* Options:
@@ -170,6 +192,16 @@ int sel_compress_zfp(sel_plan_t plan, const float *d_field, void *d_out, uint64_
  * Errors: SEL_EINVAL (NULL, options debug / kernel_timing set), SEL_ENONFINITE,
  * SEL_EDEGENERATE (status also in out->status), SEL_ENOMEM, SEL_ECUDA. */
 int sel_estimate_paper(sel_plan_t plan, const float *d_field, void *stream, sel_paper_result *out);
+
+/* N4: the log-scale and equal-probability quantisation estimates of one device
+ * field (sel_variant_result above) with the plan's eb, mode and stride: value range, the
+ * fused pass (its code histogram is the PDF), then one pass over the 65,535 bins.
+ *   log_base : integer b >= 2;  eqp_n : n in 1..32768 (2n - 1 bins).
+ * d_field: device, float32, C order; synchronises `stream`.  Errors: SEL_EINVAL (NULL,
+ * b or n out of range, options debug / kernel_timing set), SEL_ENONFINITE, SEL_EDEGENERATE
+ * (also when no code is in range; status also in out->status), SEL_ENOMEM, SEL_ECUDA. */
+int sel_estimate_variants(sel_plan_t plan, const float *d_field, int log_base, int eqp_n, void *stream,
+                          sel_variant_result *out);
 
 /* N1: the rate-distortion curve of one field at k error bounds from ONE read
  * (P:384-392 -- rate-distortion compared over error bounds; Alg. 1 lines 2-10 per eb,

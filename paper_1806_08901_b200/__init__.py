@@ -24,6 +24,7 @@ EB_ABS, EB_REL = 0, 1
 
 # every entry point declared in include/sel.h
 EXPORTS = ("sel_plan", "sel_set_option", "sel_estimate", "sel_estimate_multi", "sel_estimate_paper",
+           "sel_estimate_variants",
            "sel_compress_zfp",
            "sel_estimate_batch",
            "sel_estimate_batch_host", "sel_estimate_batch_async", "sel_choose", "sel_choose_eb",
@@ -41,6 +42,21 @@ class PaperResult(C.Structure):
         ("nsb2_total", C.c_uint64), ("n_samples", C.c_uint64), ("n_values", C.c_uint64),
         ("hist_total", C.c_uint64), ("hist_ovf", C.c_uint64), ("r_star", C.c_float),
         ("choice", C.c_int32), ("matched", C.c_int32), ("status", C.c_int32),
+    ]
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class VariantResult(C.Structure):
+    """Mirror of ``sel_variant_result`` (include/sel.h)."""
+    _fields_ = [
+        ("lin_bits", C.c_double), ("lin_psnr", C.c_double),
+        ("log_bits", C.c_double), ("log_psnr", C.c_double), ("log_mse", C.c_double),
+        ("eqp_bits", C.c_double), ("eqp_psnr", C.c_double), ("eqp_mse", C.c_double),
+        ("eqp_width_sum", C.c_double), ("value_range", C.c_double), ("eb_abs", C.c_double),
+        ("n_in", C.c_uint64), ("hist_ovf", C.c_uint64),
+        ("log_base", C.c_int32), ("log_bins", C.c_int32), ("eqp_n", C.c_int32), ("status", C.c_int32),
     ]
 
     def to_dict(self) -> dict:
@@ -94,6 +110,8 @@ def lib():
         L.sel_compress_zfp.restype = C.c_int
         L.sel_estimate_paper.argtypes = [P, P, P, C.POINTER(PaperResult)]
         L.sel_estimate_paper.restype = C.c_int
+        L.sel_estimate_variants.argtypes = [P, P, C.c_int, C.c_int, P, C.POINTER(VariantResult)]
+        L.sel_estimate_variants.restype = C.c_int
         L.sel_estimate_multi.argtypes = [P, P, C.c_int, P, P, P]
         L.sel_estimate_multi.restype = C.c_int
         L.sel_estimate_batch.argtypes = [P, P, C.c_int, P, P]
@@ -265,6 +283,14 @@ class Plan:
         r = PaperResult()
         _check(lib().sel_estimate_paper(self._h, C.c_void_p(_device_ptr(field, self.shape, self.device)),
                                         _stream_ptr(stream), C.byref(r)))
+        return r.to_dict()
+
+    def estimate_variants(self, field, log_base: int = 2, eqp_n: int = 128, stream=None) -> dict:
+        """N4: the log-scale and equal-probability quantisation estimates on the field's
+        code histogram (sel_estimate_variants)."""
+        r = VariantResult()
+        _check(lib().sel_estimate_variants(self._h, C.c_void_p(_device_ptr(field, self.shape, self.device)),
+                                           int(log_base), int(eqp_n), _stream_ptr(stream), C.byref(r)))
         return r.to_dict()
 
     def estimate_multi(self, field, ebs, stream=None) -> list[dict]:

@@ -119,6 +119,7 @@ struct sel_plan_st {
   void *zs_mem = nullptr;
   // N2 paper-literal workspace (first use): CTA partials, mid scalars, params, result
   void *paper_mem = nullptr;
+  void *var_mem = nullptr;        // N4 variant-quantiser workspace (first use)
   int paper_cap = 0;
 
   uint64_t launches = 0;
@@ -515,7 +516,7 @@ const char *sel_strerror(int status) {
   }
 }
 
-int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, int mode, double eb,
+int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, sel_eb_mode mode, double eb,
              const int32_t *stride, int32_t block) {
   if (!out || !dims || ndims < 1 || ndims > 3) return SEL_EINVAL;
   if (block != 4) return SEL_EINVAL;
@@ -804,6 +805,50 @@ int sel_estimate_paper(sel_plan_t p, const float *d_field, void *stream, sel_pap
   return SEL_OK;
 }
 
+int sel_estimate_variants(sel_plan_t p, const float *d_field, int log_base, int eqp_n, void *stream,
+                          sel_variant_result *out) {
+  if (!p || !d_field || !out || p->timing || p->debug) return SEL_EINVAL;
+  if (log_base < 2 || eqp_n < 1 || eqp_n > 32768) return SEL_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_results(p, 1);
+  if (rc) return rc;
+  if (!p->var_mem && cudaMalloc(&p->var_mem, variants_ws_bytes()) != cudaSuccess) {
+    cudaGetLastError();
+    p->var_mem = nullptr;
+    return SEL_ENOMEM;
+  }
+  Geo g = p->geo;
+  g.vec = (g.n[2] % 4 == 0) && (((uintptr_t)d_field & 15u) == 0);
+  // Alg. 1 line 2, then the fused pass of the per-field pipeline: its histogram is the PDF
+  const Workspace w = field_ws(p, 0);
+  if ((rc = launch_minmax(d_field, g.N, p->mm_ctas, w, p->mode, p->eb, st)))
+    return cuda_fail(cudaGetLastError(), "k_minmax launch");
+  const bool tile = p->tile_ok && g.vec;
+  rc = tile ? launch_tile(d_field, g, p->tl[0], w, nullptr, st)
+            : launch_estimate(d_field, g, p->el[g.vec][0], w, nullptr, st);
+  if (rc) return cuda_fail(cudaGetLastError(), "variants fused pass launch");
+  FinalizeArgs fa;
+  fa.mode = p->mode;
+  fa.eb = p->eb;
+  fa.sz_offset = p->sz_offset;
+  fa.n_sz = p->n_sz;
+  fa.n_values = p->n_values;
+  fa.n_blocks = (uint64_t)p->geo.n_pb;
+  fa.ntasks = tile ? p->tl[0].npart : p->el[g.vec][0].ntasks;
+  // the finalize copies the histogram out before it re-zeroes the workspace
+  if ((rc = launch_finalize(w, fa, p->d_res, (unsigned long long *)p->var_mem, st)))
+    return cuda_fail(cudaGetLastError(), "k_finalize launch");
+  if ((rc = launch_variants(p->var_mem, w.params, log_base, eqp_n, st)))
+    return cuda_fail(cudaGetLastError(), "k_variants launch");
+  p->launches += 4;
+  sel_variant_result h;
+  CK(cudaMemcpyAsync(&h, (char *)p->var_mem + (size_t)kNSlots * 16, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h.status != SEL_OK) return h.status;
+  *out = h;
+  return SEL_OK;
+}
+
 int sel_estimate_multi(sel_plan_t p, const float *d_field, int k, const double *ebs, void *stream,
                        sel_result *out) {
   if (!p || !d_field || !ebs || !out || k < 1 || k > kMultiMaxEb || p->timing || p->debug) return SEL_EINVAL;
@@ -1043,6 +1088,7 @@ void sel_plan_destroy(sel_plan_t p) {
   if (p->ws_mem) cudaFree(p->ws_mem);
   if (p->multi_mem) cudaFree(p->multi_mem);
   if (p->paper_mem) cudaFree(p->paper_mem);
+  if (p->var_mem) cudaFree(p->var_mem);
   if (p->zs_mem) cudaFree(p->zs_mem);
   if (p->small_mem) cudaFree(p->small_mem);
   if (p->d_res) cudaFree(p->d_res);

@@ -175,6 +175,10 @@ size_t zstream_ws_bytes(int64_t n_pb);
 int launch_zstream_bits(const float *x, const Geo &g, int sm_count, const Params *prm, void *ws,
                         unsigned long long *d_total, cudaStream_t st);
 int launch_zstream_write(const float *x, const Geo &g, const Params *prm, void *ws, uint32_t *out, cudaStream_t st);
+// N4 variant quantisers (sel_variants.cu): workspace = [hist copy | edges | result]
+size_t variants_ws_bytes();
+int launch_variants(void *vws, const Params *prm, int log_base, int eqp_n, cudaStream_t st);
+
 // N2 paper-literal estimator (sel_paper.cu)
 size_t paper_ws_bytes(int max_ctas);
 int launch_paper_zfp(const float *x, const Geo &g, int sm_count, int max_ctas, const Params *base, void *pws,

@@ -833,3 +833,87 @@ def test_small_kernel_status(sel):
             assert e.value.status == sel.SEL_ENONFINITE
         ok = p.estimate(torch.arange(256, dtype=torch.float32, device="cuda").view(16, 16))   # state was reset
         assert ok["status"] == 0
+
+
+# ---------------------------------------------------------------- N4: variant quantisers
+VAR_EXACT = ("n_in", "hist_ovf", "log_base", "log_bins", "eqp_n", "status")
+VAR_CLOSE = ("lin_bits", "lin_psnr", "log_bits", "log_psnr", "log_mse", "eqp_bits", "eqp_psnr", "eqp_mse",
+             "eqp_width_sum", "value_range", "eb_abs")
+
+
+def compare_variants(g, o, tag=""):
+    for k in VAR_EXACT:
+        assert g[k] == o[k], (tag, k, g[k], o[k])
+    for k in VAR_CLOSE:
+        assert close(float(g[k]), float(o[k])), (tag, k, g[k], o[k])
+
+
+@pytest.mark.parametrize("case", ["c1", "c2r", "c2s", "c3r", "c4s", "c5", "c5wide", "odd1d", "odd3d", "abs"])
+def test_variants_vs_oracle(sel, orc, case):
+    """sel_estimate_variants equals the oracle: the PDF's mass, the
+    overflow count and the occupied log-scale bins exactly, bit-rates / MSEs / PSNRs of the
+    linear, log-scale and equal-probability quantisers within 1e-6, for several bases and
+    bin counts, on shapes that take the tile, marching and generic fused kernels."""
+    import synth
+    mode, stride, eb = "rel", None, 1e-4
+    if case == "c1":
+        x = synth.c1_field()
+    elif case == "c2r":
+        x = synth.c2_field(0, shape=(203, 516))
+    elif case == "c2s":
+        x, stride = synth.c2_field(3, shape=(120, 400)), (1, 10)
+    elif case == "c3r":
+        x, eb = synth.c3_field(5, shape=(37, 45, 70)), 1e-5
+    elif case == "c4s":
+        x, stride = synth.c4_field(0, shape=(64, 64, 64)), (4, 4, 4)
+    elif case == "c5":
+        x, eb = synth.c5_field(1, shape=(32, 48, 64)), 1e-3
+    elif case == "c5wide":                        # codes out to the overflow slot
+        x, eb = synth.c5_field(2, shape=(32, 48, 64)), 1e-6
+    elif case == "odd1d":
+        x = np.cumsum(np.random.default_rng(3).standard_normal(10007)).astype(np.float32)
+    elif case == "odd3d":
+        x = np.cumsum(np.random.default_rng(4).standard_normal((5, 13, 27)), axis=2).astype(np.float32)
+    else:
+        rng = np.random.default_rng(5)
+        x, eb, mode = (1.0 + 0.25 * rng.standard_normal((24, 40))).astype(np.float32), 1e-3, "abs"
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    with sel.Plan(x.shape, eb, mode, stride) as p:
+        for b, n in ((2, 128), (3, 1), (10, 7), (40000, 32768), (2, 1000)):
+            o = orc.estimate_variants(x, eb, mode=mode, stride=stride, log_base=b, eqp_n=n)
+            l0 = p.launch_count
+            g = p.estimate_variants(t, b, n)
+            assert p.launch_count - l0 == 4
+            compare_variants(g, o, f"{case}/b{b}/n{n}")
+        e = p.estimate(t)                            # the plan's other entries still work after it
+    oe = orc.estimate(x, eb, mode=mode, stride=stride)
+    compare_scalars(e, oe, case + "/exact-after")
+    # the linear quantiser by the general equations is the SZ estimate itself (P:396-410)
+    if oe["hist_ovf"] == 0:
+        assert close(g["lin_bits"], e["sz_entropy"]) and close(g["lin_psnr"], e["sz_psnr"])
+
+
+def test_variants_full_size_and_errors(sel, orc):
+    """A full C3 field (100 x 500 x 500, the tile kernel) against the oracle; argument and
+    status errors."""
+    import synth
+    x = synth.make_field(3, 5)
+    o = orc.estimate_variants(x, 1e-4, log_base=2, eqp_n=128)
+    t = torch.from_numpy(x).cuda()
+    with sel.Plan(x.shape, 1e-4, "rel") as p:
+        g = p.estimate_variants(t, 2, 128)
+        compare_variants(g, o, "c3 full")
+        for b, n in ((1, 4), (2, 0), (2, 32769)):
+            with pytest.raises(sel.SelError) as ei:
+                p.estimate_variants(t, b, n)
+            assert ei.value.status == sel.SEL_EINVAL
+        bad = t.clone()
+        bad[3, 7, 9] = float("nan")
+        with pytest.raises(sel.SelError) as ei:
+            p.estimate_variants(bad, 2, 4)
+        assert ei.value.status == sel.SEL_ENONFINITE
+    c = torch.full((8, 12), 2.5, device="cuda")
+    with sel.Plan((8, 12), 1e-3, "rel") as p:
+        with pytest.raises(sel.SelError) as ei:
+            p.estimate_variants(c, 2, 4)
+        assert ei.value.status == sel.SEL_EDEGENERATE
