@@ -110,6 +110,8 @@ struct sel_plan_st {
   Params *mprm = nullptr;                         // [kMultiMaxEb]
   Partial *mpart = nullptr;                       // [kMultiMaxEb][mcap]
   int mcap = 0;                                   // CTA partials per eb
+  void *mtile_mem = nullptr;                      // tile-pipeline multi-eb pass: [task counter | partials]
+  int use_multi_tile = 1;                         // option "multi_tile"
 
   // small-field single-launch state (first use)
   void *small_mem = nullptr;
@@ -674,6 +676,10 @@ int sel_set_option(sel_plan_t p, const char *key, double value) {
     p->use_small = value != 0.0;
     return SEL_OK;
   }
+  if (!strcmp(key, "multi_tile")) {
+    p->use_multi_tile = value != 0.0;
+    return SEL_OK;
+  }
   if (!strcmp(key, "batch_kernel")) {
     p->use_batch = value != 0.0;
     return SEL_OK;
@@ -862,20 +868,40 @@ int sel_estimate_multi(sel_plan_t p, const float *d_field, int k, const double *
   if ((rc = ensure_multi(p))) return rc;
   Geo g = p->geo;
   g.vec = (g.n[2] % 4 == 0) && (((uintptr_t)d_field & 15u) == 0);
+  // full-field 2D / 3D: the TMA tile pipeline with the eb loop inside (k_tile_multi)
+  const long long tparts = p->tile_ok ? multi_tile_parts(g, p->tl[0]) : 0;
+  const bool tile = p->tile_ok && g.vec && p->use_multi_tile && tparts < (1LL << 31);
+  if (tile && !p->mtile_mem) {
+    if (cudaMalloc(&p->mtile_mem, 256 + sizeof(Partial) * (size_t)tparts * kMultiMaxEb) != cudaSuccess) {
+      cudaGetLastError();
+      p->mtile_mem = nullptr;
+      return SEL_ENOMEM;
+    }
+    if (cudaMemsetAsync(p->mtile_mem, 0, 256, st) != cudaSuccess) return cuda_fail(cudaGetLastError(), "multi tile state");
+  }
   int ctas = 0;
-  if ((rc = multi_ctas(g, k, p->sm_count, &ctas))) return cuda_fail(cudaGetLastError(), "multi occupancy");
-  if (ctas > p->mcap) ctas = p->mcap;
+  if (!tile) {
+    if ((rc = multi_ctas(g, k, p->sm_count, &ctas))) return cuda_fail(cudaGetLastError(), "multi occupancy");
+    if (ctas > p->mcap) ctas = p->mcap;
+  }
   // value range once (K1 writes vmin / vmax / non-finite into the plan's params slot)
   const Workspace w0 = field_ws(p, 0);
   if ((rc = launch_minmax(d_field, g.N, p->mm_ctas, w0, p->mode, p->eb, st)))
     return cuda_fail(cudaGetLastError(), "k_minmax launch");
-  if ((rc = launch_multi(d_field, g, ctas, k, ebs, p->mode, w0.params, p->mprm, p->mws[0].hist, p->mpart, st)))
+  Partial *const tpart = tile ? (Partial *)((char *)p->mtile_mem + 256) : nullptr;
+  if (tile) {
+    if ((rc = launch_multi_tile(d_field, g, p->tl[0], p->sm_count, k, ebs, p->mode, w0.params, p->mprm,
+                                p->mws[0].hist, tpart, (size_t)tparts, (unsigned int *)p->mtile_mem, st)))
+      return rc == SEL_ECUDA ? cuda_fail(cudaGetLastError(), "k_tile_multi launch") : rc;
+  } else if ((rc = launch_multi(d_field, g, ctas, k, ebs, p->mode, w0.params, p->mprm, p->mws[0].hist, p->mpart,
+                                st))) {
     return rc == SEL_ECUDA ? cuda_fail(cudaGetLastError(), "k_multi launch") : rc;
+  }
   // the per-eb part arrays are [e][ctas] inside [e][mcap] slots: k_multi writes
   // part[e * ctas + cta] -- give every finalize its own view
   for (int e = 0; e < k; ++e) {
     Workspace w = p->mws[e];
-    w.task_part = p->mpart + (size_t)e * ctas;
+    w.task_part = tile ? tpart + (size_t)e * (size_t)tparts : p->mpart + (size_t)e * ctas;
     FinalizeArgs fa;
     fa.mode = p->mode;
     fa.eb = ebs[e];
@@ -883,7 +909,7 @@ int sel_estimate_multi(sel_plan_t p, const float *d_field, int k, const double *
     fa.n_sz = p->n_sz;
     fa.n_values = p->n_values;
     fa.n_blocks = (uint64_t)p->geo.n_pb;
-    fa.ntasks = ctas;
+    fa.ntasks = tile ? (int)tparts : ctas;
     if ((rc = launch_finalize(w, fa, p->d_res + e, nullptr, st))) return cuda_fail(cudaGetLastError(), "k_finalize launch");
   }
   p->launches += 2 + k;
@@ -1087,6 +1113,7 @@ void sel_plan_destroy(sel_plan_t p) {
   if (p->copy_stream) cudaStreamSynchronize(p->copy_stream);
   if (p->ws_mem) cudaFree(p->ws_mem);
   if (p->multi_mem) cudaFree(p->multi_mem);
+  if (p->mtile_mem) cudaFree(p->mtile_mem);
   if (p->paper_mem) cudaFree(p->paper_mem);
   if (p->var_mem) cudaFree(p->var_mem);
   if (p->zs_mem) cudaFree(p->zs_mem);

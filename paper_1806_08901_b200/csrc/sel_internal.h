@@ -190,5 +190,10 @@ constexpr int kMultiMaxEb = 8;
 int multi_ctas(const Geo &g, int k, int sm_count, int *ctas);
 int launch_multi(const float *x, const Geo &g, int ctas, int k, const double *ebs, int mode,
                  const Params *base, Params *prm, unsigned long long *hist, Partial *part, cudaStream_t st);
+// ... on the TMA tile pipeline (full-field 2D / 3D, tile_supported shapes)
+long long multi_tile_parts(const Geo &g, const TileLaunch &tl);
+int launch_multi_tile(const float *x, const Geo &g, const TileLaunch &tl, int sm_count, int k, const double *ebs,
+                      int mode, const Params *base, Params *prm, unsigned long long *hist, Partial *part,
+                      size_t part_stride, unsigned int *task_ctr, cudaStream_t st);
 
 }  // namespace sel

@@ -14,7 +14,7 @@ __device__ __forceinline__ void bulk_ld(void *dst, const void *src, uint32_t byt
 
 template <int BG>
 __global__ void __launch_bounds__(384, 1)
-    k_mb(int iters, float r_f, int minexp, const float *gsrc, size_t gn, unsigned int *gh, unsigned long long *sink) {
+    k_mb(int iters, float r_f, int minexp, const float *gsrc, size_t gn, unsigned int *gh, unsigned long long *sink, TileGeo tg, int3 tc) {
   using Cfg = TileCfg<3>;
   extern __shared__ __align__(128) float sm[];
   float *S = sm;
@@ -70,17 +70,13 @@ __global__ void __launch_bounds__(384, 1)
     }
     return;
   }
-  TileGeo tg;
-  tg.n[0] = 1 << 20; tg.n[1] = 1 << 20; tg.n[2] = 1 << 20;
-  tg.nb[0] = 1 << 18; tg.nb[1] = 1 << 18; tg.nb[2] = 1 << 18;
-  tg.ntj = 1 << 10; tg.ntk = 1 << 10; tg.ntasks = 1 << 20;
   DebugPtrs nd{};
   unsigned int ovf = 0;
   unsigned long long acc = 0;
   double eacc = 0.0;
   for (int it = 0; it < iters; ++it) {
     uint64_t tb; double te;
-    tile_consume<3, false, unsigned int>(S, 1 + (it & 1), 1, 1, tg, warp, lane, true, r_f, minexp, win, gh, ovf, nd, tb, te);
+    tile_consume<3, false, unsigned int>(S, tc.x + (it & 1), tc.y, tc.z, tg, warp, lane, true, r_f, minexp, win, gh, ovf, nd, tb, te);
     acc += tb; eacc += te;
   }
   asm volatile("bar.sync 1, 256;");
@@ -98,11 +94,16 @@ void run(const float *gsrc, size_t gn, const char *label) {
   cudaMalloc(&gh, 70000 * 4);
   cudaMalloc(&sink, (1 + 148 * 384) * 8);
   const int iters = 200;
-  k_mb<BG><<<148, 384, smem>>>(10, 2000.f, -12, gsrc, gn, gh, sink);
+  TileGeo tg;
+  tg.n[0] = 1 << 20; tg.n[1] = 1 << 20; tg.n[2] = 1 << 20;
+  tg.nb[0] = 1 << 18; tg.nb[1] = 1 << 18; tg.nb[2] = 1 << 18;
+  tg.ntj = 1 << 10; tg.ntk = 1 << 10; tg.ntasks = 1 << 20;
+  const int3 tc = make_int3(1, 1, 1);
+  k_mb<BG><<<148, 384, smem>>>(10, 2000.f, -12, gsrc, gn, gh, sink, tg, tc);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k_mb<BG><<<148, 384, smem>>>(iters, 2000.f, -12, gsrc, gn, gh, sink);
+  k_mb<BG><<<148, 384, smem>>>(iters, 2000.f, -12, gsrc, gn, gh, sink, tg, tc);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;

@@ -10,7 +10,7 @@
 using namespace sel;
 
 #ifndef RZ
-#define RZ 152
+#define RZ 144
 #endif
 #ifndef RZ4
 #define RZ4 200
@@ -129,8 +129,8 @@ int main() {
   run<0>(2000.f, -12, 1.0f, 1e-3f, "both, 8 warps smooth");
   run<1>(2000.f, -12, 1.0f, 1e-3f, "SZ only, 8 warps");
   run<2>(2000.f, -12, 1.0f, 1e-3f, "ZFP only, 8 warps");
-  run<3>(2000.f, -12, 1.0f, 1e-3f, "8 SZ + 8 ZFP warps");
   run<4>(2000.f, -12, 1.0f, 1e-3f, "4 SZ + 8 ZFP warps");
+  run<3>(2000.f, -12, 1.0f, 1e-3f, "8 SZ + 8 ZFP warps");
   run<0>(2000.f, -12, 1.0f, 0.05f, "both, noise +-100");
   run<4>(2000.f, -12, 1.0f, 0.05f, "4+8, noise +-100");
   run<3>(2000.f, -12, 1.0f, 0.05f, "8+8, noise +-100");

@@ -583,7 +583,8 @@ def test_full_config5_fields(sel, orc, mix):
 
 
 # ---------------------------------------------------------------- N1: multi-eb in one read
-@pytest.mark.parametrize("case", ["c3", "c5", "c2", "c2s", "c4s", "odd1d", "odd3d", "abs"])
+@pytest.mark.parametrize("case", ["c3", "c5", "c2", "c2s", "c4s", "odd1d", "odd3d", "abs", "t3edge", "t2edge",
+                                  "t3k8", "t3one"])
 def test_multi_eb_vs_oracle(sel, orc, case):
     """sel_estimate_multi (one read, k ebs) equals the oracle's single-eb estimate at every
     eb: exact integer keys (histogram total / overflow, ZFP bits, minexp, choices), the
@@ -606,6 +607,14 @@ def test_multi_eb_vs_oracle(sel, orc, case):
     elif case == "odd3d":
         rng = np.random.default_rng(12)
         x, ebs = np.cumsum(rng.standard_normal((9, 14, 21)), axis=2).astype(np.float32), [1e-2, 1e-5]
+    elif case == "t3edge":       # tile pipeline (fastest extent % 4 == 0), ragged far edges, several tiles
+        x, ebs = synth.c3_field(5, shape=(37, 45, 136)), [1e-3, 1e-4, 1e-5]
+    elif case == "t2edge":
+        x, ebs = synth.c2_field(3, shape=(203, 516)), [1e-2, 1e-4, 1e-6]
+    elif case == "t3k8":         # 8 ebs: the smallest windows, equal ebs, an unsorted list
+        x, ebs = synth.c5_field(1, shape=(24, 40, 260)), [1e-4, 1e-2, 1e-3, 1e-3, 1e-6, 1e-5, 3e-4, 1e-7]
+    elif case == "t3one":
+        x, ebs = synth.c4_field(0, shape=(32, 32, 128)), [1e-4]
     else:
         x, ebs, mode = synth.c1_field(), [0.5, 0.01, 1e-4], "abs"
     t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
@@ -614,10 +623,13 @@ def test_multi_eb_vs_oracle(sel, orc, case):
         out = p.estimate_multi(t, ebs)
         assert p.launch_count - l0 == 2 + len(ebs)        # K1, one fused pass, k finalizes
         again = p.estimate_multi(t, ebs)
+        p.set_option("multi_tile", 0)                      # the one-thread-per-block pass
+        plain = p.estimate_multi(t, ebs)
     assert out == again                                    # deterministic, state re-zeroed
-    for e, r in zip(ebs, out):
+    for e, r, q in zip(ebs, out, plain):
         o = orc.estimate(x, e, mode=mode, stride=stride)
         compare_scalars(r, o, f"multi/{case}/{e}")
+        compare_scalars(q, o, f"multi-plain/{case}/{e}")
         assert sel.choose(r) == r["choice"]
 
 
