@@ -222,15 +222,18 @@ enum { REQ_T = 1, REQ_R = 2, REQ_END = 3 };
 struct RelReq { int kind, f; unsigned int cnt, rmin, rmax, rbad; };
 constexpr int kRelQ = 16;
 
-// Range warps (3D): extra warps that stream the value range of the fields ahead of the
+// Range warps: extra warps that stream the value range of the fields ahead of the
 // tiles straight from global memory into registers (LDG.128, 32 in flight per lane), so the
 // stage ring carries tiles only and a tile loads while the previous one is computed (with R
 // tasks interleaved on a 2-stage ring every tile load waited for the tile before it).
 #ifndef SEL_RW3
 #define SEL_RW3 2
 #endif
+#ifndef SEL_RW2
+#define SEL_RW2 2              // 2D: 20 consumer warps + 2 range warps (C2 1.73 -> 1.95 TB/s; 1 or 3-4: no gain)
+#endif
 template <int D>
-constexpr int range_warps() { return D == 3 ? SEL_RW3 : 0; }
+constexpr int range_warps() { return D == 3 ? SEL_RW3 : SEL_RW2; }
 template <int D>
 constexpr int batch_threads() { return (TileCfg<D>::CW + 2 + range_warps<D>()) * 32; }   // + producer + release warp
 constexpr int kRwChunk = 16384;                // floats per range-warp chunk (64 KB)
@@ -1060,7 +1063,8 @@ int launch_batch(const Geo &g, const TileLaunch &tl, const BatchSizes &bs, const
   const int nT = batch_ntasks(g, tl, bs);
   const bool sampled = g.s[0] > 1 || g.s[1] > 1 || g.s[2] > 1;
   // range warps (3D full-field stacks): no R tasks in the sequence
-  const bool rw = range_warps_on && !sampled && g.ndims == 3 && range_warps<3>() > 0;
+  const bool rw = range_warps_on && !sampled &&
+                  (g.ndims == 3 ? range_warps<3>() > 0 : g.ndims == 2 && range_warps<2>() > 0);
   const int nRs = rw ? 0 : bs.nR;
   // the histogram ring first, at a fixed offset: its slots stay zero between launches
   const size_t nslot = (size_t)G * kRing;
