@@ -466,7 +466,7 @@ def main():
         rms = max_over_ranks(world, r0.elapsed_time(r1)) / rsteps
         rv = world * field_bytes / (rms * 1e-3) / 1e9
         rd = {"ebs_rel": rd_ebs, "value": rv, "unit": "GB/s", "eb_estimates_gbs": rv * len(rd_ebs),
-              "ms_per_step": rms, "entry": "sel_estimate_multi per field (k_minmax + k_multi + k finalizes)"}
+              "ms_per_step": rms, "entry": "sel_estimate_multi per field (k_minmax + k_tile_multi + k finalizes: the value range and ONE fused pass for the k estimates)"}
         mp.close()
 
     # ---- SURVEY 8(f) N2 / N3 on the same fields: the paper-literal estimate (Alg. 1 as
@@ -530,6 +530,17 @@ def main():
         traffic = tr.get(key, {}).get(names[dom])
     except Exception:
         pass
+    # issue-slot view of the same launch (context, not the headline: DESIGN.md section 5
+    # "Issue-slot view"): the thread instructions per value the method needs (counted from
+    # the ncu opcode histogram) against the SM's issue rate, 4 warp instructions per clock
+    alu = None
+    if batch_kernel and min(st) == 1 and len(shape) in (2, 3) and clocks and clocks.get("sm_max_mhz"):
+        need = {2: 30.0, 3: 36.0}[len(shape)]
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        alu_peak = sms * 128 * clocks["sm_max_mhz"] * 1e6 / 1e12
+        alu_ach = need * int(np.prod(shape)) * nf / (avg_ms * 1e-3) / 1e12
+        alu = {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "T thread-instr/s",
+               "frac": alu_ach / alu_peak, "needed_thread_instr_per_value": need}
     cpu, parity = None, None
     if not args.no_cpu_baseline and world == 1:
         cpu, parity = cpu_baseline_and_parity(host, results, eb, st)
@@ -552,7 +563,7 @@ def main():
                      "frac": achieved / peak, "traffic": traffic, "kernel": names[dom],
                      "peak_source": peak_kind,
                      "kernel_ms": {names[k]: kms[k] / max(kcnt[k], 1) for k in range(3) if kcnt[k]},
-                     "alg_bytes_per_launch": alg_bytes},
+                     "alg_bytes_per_launch": alg_bytes, "issue_view": alu},
         "cpu_baseline": cpu,
         "parity": parity,
         "e2e": e2e,
