@@ -230,7 +230,7 @@ constexpr int kRelQ = 16;
 #define SEL_RW3 2
 #endif
 #ifndef SEL_RW2
-#define SEL_RW2 2              // 2D: 20 consumer warps + 2 range warps (C2 1.73 -> 1.95 TB/s; 1 or 3-4: no gain)
+#define SEL_RW2 2              // 2D: 2 range warps (C2 1.73 -> 1.95 TB/s with 20 consumer warps, 1.92 with 16 -- kept: stride (1,10) 2.41 -> 3.04; 1 or 3-4 range warps: no gain)
 #endif
 template <int D>
 constexpr int range_warps() { return D == 3 ? SEL_RW3 : SEL_RW2; }

@@ -12,7 +12,7 @@ namespace sel {
 
 // tile configuration (developer overrides for sweeps: -DSEL_CW2=... etc.)
 #ifndef SEL_CW2
-#define SEL_CW2 20             // (+ producer, release and 2 range warps in k_batch: 24 warps at 80 registers)
+#define SEL_CW2 16             // (+ producer, release and 2 range warps in k_batch: 20 warps at 96 registers)
 #endif
 #ifndef SEL_STAGES2
 #define SEL_STAGES2 2

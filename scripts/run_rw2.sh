@@ -1,3 +1,6 @@
-for o in "" "lag=1" "groups=1" "groups=1,lag=1" "groups=2,lag=1" "groups=3,lag=1" "groups=3" "groups=8" "groups=8,lag=1"; do
-  echo "  opts: $o"; SEL_OPTS="$o" timeout 300 python scripts/measure_all.py c2 2>&1 | grep "C2" | head -1
+for v in "-DSEL_CW2=18 -DSEL_RW2=2" "-DSEL_CW2=16 -DSEL_RW2=2 -DSEL_STAGES2=3 -DSEL_W2=4096" "-DSEL_CW2=16 -DSEL_RW2=2 -DSEL_BR2=3"; do
+  SEL_EXTRA_NVCC_FLAGS="$v" python -m paper_1806_08901_b200.build > /dev/null 2>&1 || { echo "build failed: $v"; continue; }
+  echo "== $v"
+  timeout 300 python scripts/measure_all.py c2 2>&1 | grep "^| C"
 done
+python -m paper_1806_08901_b200.build > /dev/null 2>&1
