@@ -583,7 +583,7 @@ static cudaError_t launch_pdl(const void *fn, dim3 grid, dim3 block, size_t smem
 // persistent fused-pass CTA, so the batch pipeline can overlap the two.
 int minmax_ctas(int64_t N, int sm_count) {
   int64_t want = (N + 256 * 32 - 1) / (256 * 32);
-  int64_t cap = sm_count;
+  int64_t cap = 4 * (int64_t)sm_count;   // 4 CTAs per SM: 128 KB of loads in flight per SM
   return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
