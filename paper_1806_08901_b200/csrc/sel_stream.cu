@@ -107,17 +107,21 @@ __global__ void __launch_bounds__(1024) k_scan_top(unsigned long long *csum, int
   if (threadIdx.x == 0) *total = carry;
 }
 
-// bit writer into 32-bit words (LSB first); a block's first / last word may be shared
+// bit writer into 32-bit words (LSB first) of a zeroed buffer; a block's first word (when
+// the block does not start on a word boundary) and its last, partial word may be shared
+// with its neighbours: atomicOr; every word in between is the block's own: a plain store
 struct BitWriter {
   uint32_t *out;
   unsigned long long word;
   int off;                      // bits of cur already filled (0..31)
   unsigned long long cur;
+  bool shared_word;             // the word being filled started before this block
   __device__ __forceinline__ void init(uint32_t *o, unsigned long long pos) {
     out = o;
     word = pos >> 5;
     off = (int)(pos & 31);
     cur = 0ull;
+    shared_word = off != 0;
   }
   __device__ __forceinline__ void put(uint32_t v, int n) {   // n <= 32 bits of v
     if (n <= 0) return;
@@ -125,7 +129,9 @@ struct BitWriter {
     cur |= ((unsigned long long)v & m) << off;
     off += n;
     if (off >= 32) {
-      atomicOr(out + word, (uint32_t)cur);
+      if (shared_word) atomicOr(out + word, (uint32_t)cur);
+      else out[word] = (uint32_t)cur;
+      shared_word = false;
       cur >>= 32;
       off -= 32;
       ++word;
@@ -217,9 +223,17 @@ __global__ void __launch_bounds__(256) k_zwrite(const float *__restrict__ x, Geo
       const int kmin = 32 - prec;
       int n = 0;                               // coefficients already significant
       for (int kp = 31; kp >= kmin; --kp) {
-        unsigned long long mask = 0ull;        // bit plane kp over the sequency order
+        // bit plane kp over the sequency order: the planes are visited from the top, so the
+        // plane's bit of u[j] is its current top bit -- one funnel shift moves it into the
+        // mask, one add drops it (2 instructions per coefficient and plane)
+        uint32_t mlo = 0u, mhi = 0u;
 #pragma unroll
-        for (int j = 0; j < SZ; ++j) mask |= (unsigned long long)((u[j] >> kp) & 1u) << j;
+        for (int j = SZ - 1; j >= 0; --j) {
+          if (j >= 32) mhi = __funnelshift_l(u[j], mhi, 1);
+          else mlo = __funnelshift_l(u[j], mlo, 1);
+          u[j] += u[j];
+        }
+        const unsigned long long mask = ((unsigned long long)mhi << 32) | mlo;
         bw.put64(mask, n);                     // (i) bits of 0..n-1 verbatim
         while (n < SZ) {                       // (ii) group tests
           const unsigned long long rest = mask >> n;
