@@ -19,6 +19,7 @@ def run(fields, eb, stride, label):
         if kv:
             p.set_option(kv.split("=")[0], float(kv.split("=")[1]))
     buf = p.results_buffer(len(fields))
+    nfields, fields = len(fields), p.field_stack(fields)      # pointers marshalled once
     for _ in range(2):
         p.estimate_batch_async(fields, buf)
     torch.cuda.synchronize()
@@ -30,7 +31,7 @@ def run(fields, eb, stride, label):
     ms = e0.elapsed_time(e1) / 5
     res = p.decode_results(buf, len(fields))
     nsz = sum(1 for r in res if r["choice"] == 0)
-    gbs = len(fields) * fields[0].numel() * 4 / ms / 1e6
+    gbs = len(fields) * fields.fields[0].numel() * 4 / ms / 1e6
     print(f"| {label} | {len(fields)} | {eb:g} | {stride or 'all'} | {ms / len(fields) * 1e3:.1f} | "
           f"{gbs:.0f} | {100 * gbs / PEAK:.1f} | {nsz} / {len(fields) - nsz} |", flush=True)
     p.close()

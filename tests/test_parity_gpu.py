@@ -929,3 +929,21 @@ def test_variants_full_size_and_errors(sel, orc):
         with pytest.raises(sel.SelError) as ei:
             p.estimate_variants(c, 2, 4)
         assert ei.value.status == sel.SEL_EDEGENERATE
+
+
+def test_field_stack_equals_list(sel):
+    """Plan.field_stack (pointers marshalled once) gives the same results as the list form,
+    sync and async, and validates shapes like the list form."""
+    import synth
+    xs = [torch.from_numpy(synth.c1_field(seed=i)).cuda() for i in range(5)]
+    with sel.Plan((256, 256), 1e-4) as p:
+        ref = p.estimate_batch(xs)
+        stk = p.field_stack(xs)
+        assert len(stk) == 5
+        assert p.estimate_batch(stk) == ref
+        buf = p.results_buffer(5)
+        p.estimate_batch_async(stk, buf)
+        torch.cuda.synchronize()
+        assert p.decode_results(buf, 5) == ref
+        with pytest.raises(ValueError):
+            p.field_stack([xs[0], torch.zeros(8, 8, device="cuda")])
