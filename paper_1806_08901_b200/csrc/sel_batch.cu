@@ -227,7 +227,7 @@ constexpr int kRelQ = 16;
 // stage ring carries tiles only and a tile loads while the previous one is computed (with R
 // tasks interleaved on a 2-stage ring every tile load waited for the tile before it).
 #ifndef SEL_RW3
-#define SEL_RW3 2
+#define SEL_RW3 1              // 3D: one range warp (C4 1.59 -> 1.62 TB/s, C3 +2-3 % against two; waiting consumers help)
 #endif
 #ifndef SEL_RW2
 #define SEL_RW2 2              // 2D: 2 range warps (C2 1.73 -> 1.95 TB/s with 20 consumer warps, 1.92 with 16 -- kept: stride (1,10) 2.41 -> 3.04; 1 or 3-4 range warps: no gain)

@@ -1,6 +1,6 @@
-for v in "-DSEL_CW2=18 -DSEL_RW2=2" "-DSEL_CW2=16 -DSEL_RW2=2 -DSEL_STAGES2=3 -DSEL_W2=4096" "-DSEL_CW2=16 -DSEL_RW2=2 -DSEL_BR2=3"; do
+for v in "-DSEL_RW3=1" "-DSEL_W3=8192"; do
   SEL_EXTRA_NVCC_FLAGS="$v" python -m paper_1806_08901_b200.build > /dev/null 2>&1 || { echo "build failed: $v"; continue; }
   echo "== $v"
-  timeout 300 python scripts/measure_all.py c2 2>&1 | grep "^| C"
+  timeout 300 python scripts/measure_all.py c3,c4 2>&1 | grep "^| C" | grep -v "N1\|(4, 4"
 done
 python -m paper_1806_08901_b200.build > /dev/null 2>&1
