@@ -158,6 +158,11 @@ int sel_plan(sel_plan_t *out, int ndims, const int64_t *dims, sel_eb_mode mode, 
  *   "groups"          k_batch CTA groups, 0 (default) = automatic, else 1..148
  *   "lag"             k_batch phases between a field's range pass and its tiles, 1..4
  *                     (default 2)
+ *   "range_warps"     1 (default) = k_batch streams the value range of full-field stacks on
+ *                     dedicated warps; 0 = as range tasks through the tile stage ring
+ *   "small_kernel"    1 (default) = one small field (N <= 2^21) in one cooperative launch
+ *   "multi_tile"      1 (default) = sel_estimate_multi runs its fused pass on the TMA tile
+ *                     pipeline where the shape allows; 0 = one thread per block
  *   "batch_debug"     1 = the persistent k_batch kernel also dumps, per field, the
  *                     histogram its finalize tasks read and its per-(task, part) partials
  *                     (sel_debug_copy "batch_hist" / "batch_part"; tests)
@@ -209,7 +214,9 @@ int sel_estimate_variants(sel_plan_t plan, const float *d_field, int log_base, i
  * mode (absolute, or x value range); dims, stride and block are the plan's.  The value
  * range is computed once, every processed block is read once, its Lorenzo residuals and
  * ZFP transform are formed once, and the eb-dependent stages (quantisation + histogram,
- * fixed-accuracy cut, bit count, error) run per eb.  out[e] (host, k entries) equals what
+ * fixed-accuracy cut, bit count, error) run per eb (full-field 2D / 3D shapes with the
+ * fastest extent % 4 == 0 and a 16-byte aligned field: on the TMA tile pipeline, one
+ * shared-memory histogram window per eb).  out[e] (host, k entries) equals what
  * sel_estimate would return at ebs[e] (per-eb status in out[e].status: SEL_ENONFINITE,
  * SEL_EDEGENERATE, ...).  d_field: device, float32, C order, not modified; the call
  * synchronises `stream`.  Errors: SEL_EINVAL (NULL, k out of range, eb not finite or <= 0,
